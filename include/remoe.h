@@ -1,0 +1,190 @@
+/*
+ * remoe.h -- C ABI of the B200-native Similar Prompts Searching (SPS) predictor.
+ *
+ * Paper: "Remoe: Towards Efficient and Low-Cost MoE Inference in Serverless
+ * Computing", arXiv 2512.18674.  Line citations "P:n" are PAPER.md
+ * lines; "S:n" are SPEC.md lines; "DESIGN R<n>" are the readings listed in
+ * DESIGN.md where the paper is silent or ambiguous.
+ *
+ * What the library computes (the data-parallel hot path):
+ *
+ *   score(q, x_j) = (q . x_j) / (|q| |x_j| + sigma)                     (S1-S2)
+ *       Eq. 11.  The paper's SCS on token matrices equals the
+ *       cosine of the summed L2-normalised token rows (DESIGN R2), so a
+ *       "prompt embedding" here is that sum (or any positive rescaling).
+ *   top-k over all stored prompts, ordered by score descending, then global
+ *       id ascending (DESIGN R5)                                          (S3-S5)
+ *       Exact brute force, the paper's "BF"; k is the paper's alpha.
+ *   w_r = softmax(s_r / T) over the k retrieved scores                   (S6)
+ *       P:421 "converted into probability weights via softmax" (T=1, DESIGN R4).
+ *   P[l][e] = sum_r w_r * S~_{id_r}[l][e], r = 0..k-1 ascending           (S7)
+ *       P:421 "weighted-summed to predict the result"; S~ rows are the
+ *       "linear scaling activation frequencies" of P:420.
+ *   cold[l][e] = 1 for the n_cold experts of layer l with the smallest P   (S8)
+ *       P:504 remote-expert selection: u_{l,k} = N_in s~ + N_out N_topk s~
+ *       is a positive multiple of s~, so argmin of sum u over |R_l| = b K_l
+ *       picks the n_cold smallest s~ (ties: lower expert index, DESIGN R12).
+ *
+ * Precision: embeddings and queries are bf16; dot products accumulate in fp32
+ * (tensor-core or FMA) in an order fixed per (query, row) and independent of
+ * the query's batch position and of the sharding; norms, scores, weights and
+ * predictions are fp32.  Selection is exact with respect to the fp32 scores
+ * and the key order above.
+ *
+ * Conventions (all functions):
+ *   - C linkage, no exception or abort crosses the boundary.
+ *   - Argument errors are detected synchronously, before any launch, and
+ *     return REMOE_ERR_INVALID_ARG (or REMOE_ERR_UNSUPPORTED for legal but
+ *     unimplemented shapes); outputs are then untouched.
+ *   - Device work is asynchronous on the caller's stream; asynchronous CUDA /
+ *     NCCL faults surface at the next call or at remoe_sps_sync().
+ *   - remoe_last_error() returns a thread-local description of the last failure.
+ *   - A handle is not safe for concurrent calls from several threads.
+ */
+#ifndef REMOE_H_
+#define REMOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define REMOE_API __attribute__((visibility("default")))
+#else
+#define REMOE_API
+#endif
+
+typedef enum {
+  REMOE_OK = 0,
+  REMOE_ERR_INVALID_ARG = 1, /* bad pointer, size, shard tiling, k > N_total, ... */
+  REMOE_ERR_CUDA = 2,        /* a CUDA runtime/driver call failed */
+  REMOE_ERR_NCCL = 3,        /* an NCCL call failed (multi-GPU only) */
+  REMOE_ERR_OOM = 4,         /* device allocation failed */
+  REMOE_ERR_UNSUPPORTED = 5, /* legal but not implemented (e.g. k > 256, D > 4096) */
+  REMOE_ERR_STATE = 6        /* handle misuse (NULL handle, destroyed, wrong device) */
+} remoe_status_t;
+
+typedef struct remoe_sps* remoe_sps_t; /* opaque, library-owned */
+
+/*
+ * Build configuration.  One per rank; the store is sharded row-wise into
+ * contiguous ranges: rank g owns global rows [global_offset, global_offset +
+ * n_local), and the ranges of ranks 0..world-1 must tile [0, N_total) in rank
+ * order (checked at build when world > 1; INVALID_ARG otherwise).
+ */
+typedef struct {
+  int64_t n_local;        /* rows on this rank (>= 1) */
+  int64_t global_offset;  /* global id of this rank's first row */
+  int32_t dim;            /* D: embedding dimension, D % 8 == 0, 8 <= D <= 4096 */
+  int32_t n_layers;       /* L: MoE layers of the activation table (>= 1) */
+  int32_t n_experts;      /* E: routed experts per layer, 1 <= E <= 256 */
+  float sigma;            /* Eq. 11 guard sigma > 0; DESIGN R3 default 1e-6 */
+  float temperature;      /* softmax temperature T > 0 (DESIGN R4 default 1) */
+  int32_t max_batch;      /* workspace sizing: largest B per internal chunk (>= 1) */
+  int32_t max_k;          /* largest k ever queried, 1 <= max_k <= 256 */
+  int32_t device;         /* CUDA device ordinal this handle lives on */
+  int32_t rank, world;    /* 0 <= rank < world; world == 1 => no NCCL */
+  const void* nccl_unique_id; /* 128-byte ncclUniqueId identical on all ranks; NULL iff world == 1 */
+  int32_t inputs_on_device;   /* 1: emb/act passed to build are device pointers on `device`; 0: host */
+  int32_t validate;       /* 1: reject non-finite embeddings, act < 0, |row sum - 1| > 1e-3 */
+} remoe_sps_config_t;
+
+/* Fill *cfg with defaults (sigma 1e-6, T 1, max_batch 256, max_k 128, world 1,
+ * validate 1); the caller then sets n_local, dim, n_layers, n_experts, ... */
+REMOE_API void remoe_sps_config_default(remoe_sps_config_t* cfg);
+
+/*
+ * S0: ingest this rank's shard of the history.
+ *   emb_bf16: [n_local x dim] row-major bf16 bit patterns (prompt vectors,
+ *             P:374-385).  Copied; the caller keeps ownership.
+ *   act:      [n_local x L x E] fp32 row-stochastic per (prompt, layer) activation
+ *             frequencies S~.  Copied; the caller keeps ownership.
+ *   out:      receives the handle on success, NULL on failure.
+ * Collective over `world` ranks (all ranks must call it).  Synchronous: returns
+ * after the device copies and the |x_j| pass have completed.
+ */
+REMOE_API remoe_status_t remoe_sps_build(const remoe_sps_config_t* cfg, const uint16_t* emb_bf16,
+                                         const float* act, remoe_sps_t* out);
+
+/*
+ * S1-S7: score B queries against the whole (sharded) store, return the global
+ * top-k and the predicted activation matrix.
+ *   q_bf16: device [B x dim] bf16 bits, identical on every rank (SPMD).
+ *   B >= 0 (B == 0 is a no-op), 1 <= k <= min(N_total, max_k).  B > max_batch
+ *   is processed in internal chunks of max_batch.
+ *   ids:    device [B x k] int64 global ids, by score desc then id asc.
+ *   scores: device [B x k] fp32 scores (Eq. 11).
+ *   pred:   device [B x L x E] fp32 prediction, or NULL to skip S6-S7.
+ *   stream: the caller's stream; all work is enqueued there.
+ * Collective when world > 1: every rank must call with the same B, k and
+ * queries, and every rank receives identical outputs.
+ */
+REMOE_API remoe_status_t remoe_sps_query(remoe_sps_t h, const uint16_t* q_bf16, int32_t B,
+                                         int32_t k, int64_t* ids, float* scores, float* pred,
+                                         void* stream);
+
+/*
+ * Same as remoe_sps_query, but q/ids/scores/pred are HOST buffers (pinned or
+ * pageable).  Copies in, runs, copies out and synchronizes the stream before
+ * returning.  This is the end-to-end entry point a serving front end calls.
+ */
+REMOE_API remoe_status_t remoe_sps_query_host(remoe_sps_t h, const uint16_t* q_bf16, int32_t B,
+                                              int32_t k, int64_t* ids, float* scores, float* pred,
+                                              void* stream);
+
+/*
+ * S8: remote-expert selection.  For each (query b, layer l), the n_cold
+ * experts with the smallest pred[b][l][e] (ties -> lower e) get mask 1 (cold /
+ * remote, x_{l,k} = 1), the rest 0 (hot / local).
+ *   pred: device [B x L x E] fp32; cold_mask: device [B x L x E] uint8.
+ *   0 <= n_cold <= E (n_cold = floor(b * E) for MMP's remote ratio b).
+ * Stateless; no communication.
+ */
+REMOE_API remoe_status_t remoe_expert_plan(const float* pred, int32_t B, int32_t L, int32_t E,
+                                           int32_t n_cold, uint8_t* cold_mask, void* stream);
+
+/* Rank 0 calls this, then broadcasts the 128 bytes to all ranks (e.g. as a uint8
+ * tensor over a torch.distributed group) before remoe_sps_build. */
+REMOE_API remoe_status_t remoe_nccl_unique_id(uint8_t out[128]);
+
+/* Synchronize the handle's device work and surface asynchronous CUDA/NCCL errors. */
+REMOE_API remoe_status_t remoe_sps_sync(remoe_sps_t h);
+
+/* Introspection: N_total, the kernel the last query used, and workspace bytes. */
+typedef struct {
+  int64_t n_total, n_local, global_offset;
+  int32_t dim, n_layers, n_experts, rank, world;
+  int32_t last_scan_kernel;   /* 0 none, 1 streaming (CUDA cores), 2 tensor core (tcgen05) */
+  int32_t last_launches;      /* kernels launched by the last query (all chunks) */
+  int32_t scan_ctas;          /* grid of the scan kernel */
+  int64_t device_bytes;       /* store + table + workspaces */
+} remoe_sps_info_t;
+REMOE_API remoe_status_t remoe_sps_get_info(remoe_sps_t h, remoe_sps_info_t* info);
+
+/* Force the scan kernel: 0 auto (default), 1 streaming, 2 tensor core.
+ * Also settable with the environment variable REMOE_FORCE_KERNEL=stream|tc. */
+REMOE_API remoe_status_t remoe_sps_set_kernel(remoe_sps_t h, int32_t which);
+
+/*
+ * Live kernel timing for benchmarks.  enable = 1 starts recording CUDA events on
+ * the query stream around every scan-kernel launch (S2+S3); each call returns
+ * (after synchronizing those events) the accumulated scan time in ms and the
+ * number of scan launches since the previous call, then resets them.
+ * enable = 0 stops recording.  scan_ms / launches may be NULL.
+ */
+REMOE_API remoe_status_t remoe_sps_profile(remoe_sps_t h, int32_t enable, double* scan_ms,
+                                           int64_t* launches);
+
+/* Collective when world > 1.  NULL-safe. */
+REMOE_API void remoe_sps_destroy(remoe_sps_t h);
+
+REMOE_API const char* remoe_status_string(remoe_status_t s);
+REMOE_API const char* remoe_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* REMOE_H_ */

@@ -1,0 +1,245 @@
+// common.cuh -- device primitives shared by the SPS kernels (sm_100a).
+//
+// * Candidate keys: u64 = ordf(fp32 score) << 32 | (0xFFFFFFFF - gid).
+//   The larger key is the better candidate: score descending, then global id
+//   ascending (DESIGN R5).  Key 0 is the "no candidate" sentinel; every real key
+//   is >= 1.  -0.0 is canonicalised to +0.0 before packing.
+// * Warp bitonic sort of 32*P keys held P per lane (index i = lane*P + p).
+// * Thread-private top-k ("one lane owns one query"): a threshold in a register
+//   plus an append-only buffer of CAP = 32*P keys in global memory (L2); when a
+//   lane's buffer is full the whole warp sorts it and keeps the best k.  Exact:
+//   nothing better than the k-th kept key is ever discarded.
+// * mbarrier / bulk-copy (TMA) PTX wrappers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace remoe {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+// ---------------------------------------------------------------- keys
+__device__ __forceinline__ uint32_t ordf(float f) {
+  uint32_t u = __float_as_uint(f);
+  if ((u & 0x7FFFFFFFu) == 0) u = 0;  // -0 -> +0
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float unordf(uint32_t o) {
+  return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
+}
+__device__ __forceinline__ uint64_t make_key(float s, int64_t gid) {
+  return ((uint64_t)ordf(s) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)gid);
+}
+__device__ __forceinline__ int64_t key_gid(uint64_t k) {
+  return (int64_t)(0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFull));
+}
+__device__ __forceinline__ float key_score(uint64_t k) { return unordf((uint32_t)(k >> 32)); }
+
+// Eq. 11 on fp32 pieces: dot / (|q| |x| + sigma).  One fused multiply-add
+// for the denominator and one IEEE division; identical in every kernel.
+__device__ __forceinline__ float eq11(float dot, float qn, float xn, float sigma) {
+  return __fdiv_rn(dot, __fmaf_rn(qn, xn, sigma));
+}
+
+// bf16 bit pairs packed in a 32-bit word -> fp32 (exact)
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+__device__ __forceinline__ uint64_t umax64(uint64_t a, uint64_t b) { return a > b ? a : b; }
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+// ---------------------------------------------------------------- warp bitonic sort
+// Sorts the 32*P keys of the warp in DESCENDING order; element i = lane*P + p.
+template <int P>
+__device__ __forceinline__ void warp_sort_desc(uint64_t (&v)[P]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int size = 2; size <= 32 * P; size <<= 1) {
+#pragma unroll
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      if (j >= P) {
+        const int lj = j / P;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const int i = lane * P + p;
+          const uint64_t o = __shfl_xor_sync(kFull, v[p], lj);
+          const bool up = (i & size) == 0;
+          const bool lower = (i & j) == 0;
+          v[p] = (lower == up) ? umax64(v[p], o) : umin64(v[p], o);
+        }
+      } else {
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const int q = p ^ j;
+          if (q > p) {
+            const int i = lane * P + p;
+            const uint64_t a = v[p], b = v[q];
+            if ((i & size) == 0) { v[p] = umax64(a, b); v[q] = umin64(a, b); }
+            else                 { v[p] = umin64(a, b); v[q] = umax64(a, b); }
+          }
+        }
+      }
+    }
+  }
+}
+
+// Key at sorted position `pos` (warp-uniform), broadcast to all lanes.
+template <int P>
+__device__ __forceinline__ uint64_t warp_key_at(const uint64_t (&v)[P], int pos) {
+  uint64_t mine = 0;
+#pragma unroll
+  for (int p = 0; p < P; ++p)
+    if (p == (pos % P)) mine = v[p];
+  return __shfl_sync(kFull, mine, pos / P);
+}
+
+// Sort the first `cnt` keys of buf (others read as 0) and write the best `k`
+// back to buf[0..k) (or to `out` if non-null).  Returns the k-th best key
+// (0 if cnt < k).  Whole warp, warp-uniform arguments.
+template <int P>
+__device__ __forceinline__ uint64_t warp_compact(uint64_t* buf, int cnt, int k, uint64_t* out) {
+  const int lane = threadIdx.x & 31;
+  uint64_t v[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int i = lane * P + p;
+    v[p] = i < cnt ? buf[i] : 0ull;
+  }
+  warp_sort_desc<P>(v);
+  __syncwarp();
+  uint64_t* dst = out ? out : buf;
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const int i = lane * P + p;
+    if (i < k) dst[i] = v[p];
+  }
+  __syncwarp();
+  return cnt >= k ? warp_key_at<P>(v, k - 1) : 0ull;
+}
+
+// Thread-private top-k state of one lane (one query per lane).
+template <int P>
+struct LaneTopk {
+  static constexpr int CAP = 32 * P;
+  uint64_t thr;   // every kept key is > thr once thr != 0 (k-th best after a compaction)
+  int cnt;        // keys in buf
+  uint64_t* buf;  // CAP keys, private to this lane
+
+  __device__ __forceinline__ void init(uint64_t* b) { thr = 0; cnt = 0; buf = b; }
+
+  // Whole warp calls with one key per lane (0 = nothing to offer).
+  __device__ __forceinline__ void push(uint64_t key, int k) {
+    const int lane = threadIdx.x & 31;
+    unsigned full = __ballot_sync(kFull, key > thr && cnt == CAP);
+    while (full) {
+      const int L = __ffs(full) - 1;
+      full &= full - 1;
+      uint64_t* b = (uint64_t*)__shfl_sync(kFull, (unsigned long long)buf, L);
+      const uint64_t t = warp_compact<P>(b, CAP, k, nullptr);
+      if (lane == L) { thr = t; cnt = k; }
+    }
+    if (key > thr) buf[cnt++] = key;
+  }
+
+  // Whole warp: write each lane's sorted best k to out_of(lane) (k keys, zero padded).
+  __device__ __forceinline__ void flush(uint64_t* my_out, int k) {
+    for (int L = 0; L < 32; ++L) {
+      uint64_t* b = (uint64_t*)__shfl_sync(kFull, (unsigned long long)buf, L);
+      uint64_t* o = (uint64_t*)__shfl_sync(kFull, (unsigned long long)my_out, L);
+      const int c = __shfl_sync(kFull, cnt, L);
+      if (o != nullptr) warp_compact<P>(b, c, k, o);
+    }
+  }
+};
+
+// Warp-shared top-k over a stream of keys for ONE query (all lanes feed it).
+// Buffer in shared memory; CAP = 32*P >= k + 32.
+template <int P>
+struct WarpTopk {
+  static constexpr int CAP = 32 * P;
+  uint64_t thr;
+  int cnt;
+  uint64_t* buf;
+  __device__ __forceinline__ void init(uint64_t* b) { thr = 0; cnt = 0; buf = b; }
+  __device__ __forceinline__ void push(uint64_t key, int k) {
+    const int lane = threadIdx.x & 31;
+    unsigned m = __ballot_sync(kFull, key > thr);
+    if (!m) return;
+    if (cnt + __popc(m) > CAP) {
+      thr = warp_compact<P>(buf, cnt, k, nullptr);
+      cnt = k < cnt ? k : cnt;
+      m = __ballot_sync(kFull, key > thr);
+    }
+    if (key > thr) buf[cnt + __popc(m & ((1u << lane) - 1u))] = key;
+    cnt += __popc(m);
+    __syncwarp();
+  }
+  __device__ __forceinline__ void finish(uint64_t* out, int k) {
+    warp_compact<P>(buf, cnt, k, out);
+  }
+};
+
+// ---------------------------------------------------------------- mbarrier + bulk copy
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk copy global -> shared, completion counted on `bar` (TMA engine).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint4 lds128(const void* p) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ float4 lds128f(const void* p) {
+  float4 r;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "r"(smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ uint4 ldg_nc128(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// CAP selection shared by host and device: CAP = 32*P >= max(64, pow2ceil(4k)).
+__host__ __device__ constexpr int topk_P(int k) {
+  return (4 * k <= 64) ? 2 : (4 * k <= 128) ? 4 : (4 * k <= 256) ? 8 : (4 * k <= 512) ? 16 : 32;
+}
+
+}  // namespace remoe

@@ -1,0 +1,72 @@
+// kernels.h -- launch interface of the SPS device kernels (internal to libremoe).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace remoe {
+
+// S2+S3, streaming (CUDA-core) variant.  Scores nq <= BQ queries against rows
+// [0, n_rows) of the shard; writes per-CTA sorted top-k key lists to
+// out[(query * grid + cta) * k + i] (zero padded).
+struct SimtScanParams {
+  const uint16_t* x;      // [n_rows][dim] bf16
+  const float* xnorm;     // [n_rows]
+  int64_t n_rows;
+  int64_t gid_offset;     // global id of row 0
+  int dim;
+  const uint16_t* q;      // [nq][dim] bf16
+  const float* qnorm;     // [nq]
+  int nq;
+  int k;
+  float sigma;
+  int stage_rows;         // rows per TMA stage
+  int n_stages_ring;      // ring depth
+  uint64_t* cand_buf;     // [grid][32][CAP] private lane buffers
+  uint64_t* out;          // [nq][grid][k]
+};
+size_t simt_smem_bytes(int BQ, int dim, int stage_rows, int n_stages_ring);
+cudaError_t launch_scan_simt(const SimtScanParams& p, int BQ, int grid, cudaStream_t st);
+
+// S2+S3, tensor-core (tcgen05) variant; see k_scan_tc.cu.
+struct TcScanParams {
+  const void* tmap_x;     // CUtensorMap* (host-encoded, passed by value via __grid_constant__)
+  const float* xnorm;
+  int64_t n_rows;
+  int64_t gid_offset;
+  int dim;
+  const uint16_t* q;      // [nq][dim]
+  const float* qnorm;
+  int nq;                 // queries in this pass (<= 128 per M tile)
+  int k;
+  float sigma;
+  uint64_t* cand_buf;
+  uint64_t* out;          // [nq][grid][k]
+};
+
+// S1 / S0: L2 norms of bf16 rows (fp32, fixed order).
+cudaError_t launch_norms(const uint16_t* x, int64_t n, int dim, float* out, cudaStream_t st);
+
+// S4 / S5: per query, merge n_lists sorted key lists of length k into the best k.
+// key(b, l, i) = in[b * qstride + l * lstride + i].
+cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride, int64_t lstride,
+                         int k, uint64_t* out, cudaStream_t st);
+
+// S6 + S7.  mode 0: rows come from the local table act[(gid - offset) * LE];
+// mode 1: rows come from rows[(b * k + r) * LE] (multi-GPU gathered winners).
+cudaError_t launch_finalize(const uint64_t* top, int B, int k, const float* act, int64_t offset,
+                            const float* rows, int mode, int64_t LE, float temperature,
+                            int64_t* ids, float* scores, float* pred, cudaStream_t st);
+
+// Multi-GPU S7 helper: rows[b][r] = act[gid - offset] if this rank owns gid, else 0.
+cudaError_t launch_gather_rows(const uint64_t* top, int B, int k, const float* act, int64_t offset,
+                               int64_t n_local, int64_t LE, float* rows, cudaStream_t st);
+
+// S8: cold mask of the n_cold smallest entries per (query, layer).
+cudaError_t launch_plan(const float* pred, int B, int L, int E, int n_cold, uint8_t* mask,
+                        cudaStream_t st);
+
+// Build-time validation: counts non-finite embeddings and bad activation rows.
+cudaError_t launch_validate(const uint16_t* x, int64_t n, int dim, const float* act, int64_t LE_rows,
+                            int E, unsigned long long* bad, cudaStream_t st);
+
+}  // namespace remoe

@@ -1,0 +1,530 @@
+// runtime.cu -- the C ABI (include/remoe.h): handle, validation, workspaces,
+// kernel selection, the per-query launch sequence and the NCCL exchange.
+//
+// Query sequence per chunk of <= max_batch queries:
+//   k_norms(Q)                                   S1
+//   k_scan_{simt|tc}                             S2+S3  (per-CTA top-k lists)
+//   k_merge(n_cta lists -> local top-k)          S4
+//   [world > 1] ncclAllGather(local keys) + k_merge(G lists -> global top-k)   S5
+//   [pred]  world == 1: k_finalize(mode 0, rows read from the local table)    S6+S7
+//           world >  1: k_gather_rows (owned winners, zeros elsewhere)
+//                       + ncclAllReduce(sum): exactly one non-zero term per
+//                         element, so the sum is exact and order-free
+//                       + k_finalize(mode 1)  -> bit-identical to world == 1
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "remoe.h"
+#include "tc_host.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+remoe_status_t fail(remoe_status_t s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(e_ == cudaErrorMemoryAllocation ? REMOE_ERR_OOM : REMOE_ERR_CUDA,        \
+                  "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__);    \
+  } while (0)
+
+#define NCCL_TRY(expr)                                                                     \
+  do {                                                                                     \
+    ncclResult_t r_ = (expr);                                                              \
+    if (r_ != ncclSuccess)                                                                 \
+      return fail(REMOE_ERR_NCCL, "%s: %s (%s:%d)", #expr, ncclGetErrorString(r_),         \
+                  __FILE__, __LINE__);                                                     \
+  } while (0)
+
+#define ST_TRY(expr)                       \
+  do {                                     \
+    remoe_status_t s_ = (expr);            \
+    if (s_ != REMOE_OK) return s_;         \
+  } while (0)
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+struct remoe_sps {
+  remoe_sps_config_t cfg{};
+  int64_t n_total = 0;
+  int64_t LE = 0;
+  int num_sms = 0;
+  int grid_simt = 0;
+  int grid_tc = 0;
+  int stage_rows = 0;
+  // store
+  uint16_t* x = nullptr;
+  float* xnorm = nullptr;
+  float* act = nullptr;
+  // workspaces
+  float* qnorm = nullptr;
+  uint64_t* cand_buf = nullptr;
+  uint64_t* lists = nullptr;
+  uint64_t* local_top = nullptr;
+  uint64_t* gathered = nullptr;
+  uint64_t* global_top = nullptr;
+  float* rows = nullptr;
+  // host-path staging
+  uint16_t* hq = nullptr;
+  int64_t* hids = nullptr;
+  float* hscores = nullptr;
+  float* hpred = nullptr;
+  // tensor-core path
+  remoe::TcPlan tc{};
+  ncclComm_t comm = nullptr;
+  int force_kernel = 0;
+  int last_kernel = 0;
+  int last_launches = 0;
+  size_t device_bytes = 0;
+  std::vector<void*> allocs;
+  // live scan timing (remoe_sps_profile)
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_ev;  // pairs (start, end)
+  size_t prof_used = 0;              // pairs recorded since the last read
+  double prof_ms = 0.0;
+  int64_t prof_launches = 0;
+
+  cudaError_t prof_mark(cudaStream_t st, bool start) {
+    if (!prof) return cudaSuccess;
+    const size_t idx = 2 * prof_used + (start ? 0 : 1);
+    while (prof_ev.size() <= idx) {
+      cudaEvent_t e;
+      cudaError_t r = cudaEventCreate(&e);
+      if (r != cudaSuccess) return r;
+      prof_ev.push_back(e);
+    }
+    cudaError_t r = cudaEventRecord(prof_ev[idx], st);
+    if (!start) ++prof_used;
+    return r;
+  }
+  cudaError_t prof_collect() {
+    for (size_t i = 0; i < prof_used; ++i) {
+      cudaError_t r = cudaEventSynchronize(prof_ev[2 * i + 1]);
+      if (r != cudaSuccess) return r;
+      float ms = 0.f;
+      r = cudaEventElapsedTime(&ms, prof_ev[2 * i], prof_ev[2 * i + 1]);
+      if (r != cudaSuccess) return r;
+      prof_ms += ms;
+    }
+    prof_used = 0;
+    return cudaSuccess;
+  }
+
+  remoe_status_t alloc(void** p, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess)
+      return fail(e == cudaErrorMemoryAllocation ? REMOE_ERR_OOM : REMOE_ERR_CUDA,
+                  "cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+    allocs.push_back(*p);
+    device_bytes += bytes;
+    return REMOE_OK;
+  }
+  void release() {
+    for (void* p : allocs) cudaFree(p);
+    allocs.clear();
+    for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
+    prof_ev.clear();
+    remoe::tc_plan_destroy(&tc);
+    if (comm) { ncclCommDestroy(comm); comm = nullptr; }
+  }
+};
+
+extern "C" {
+
+void remoe_sps_config_default(remoe_sps_config_t* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof *c);
+  c->sigma = 1e-6f;
+  c->temperature = 1.0f;
+  c->max_batch = 256;
+  c->max_k = 128;
+  c->world = 1;
+  c->validate = 1;
+}
+
+const char* remoe_status_string(remoe_status_t s) {
+  switch (s) {
+    case REMOE_OK: return "ok";
+    case REMOE_ERR_INVALID_ARG: return "invalid argument";
+    case REMOE_ERR_CUDA: return "CUDA error";
+    case REMOE_ERR_NCCL: return "NCCL error";
+    case REMOE_ERR_OOM: return "out of device memory";
+    case REMOE_ERR_UNSUPPORTED: return "unsupported";
+    case REMOE_ERR_STATE: return "invalid state";
+  }
+  return "unknown status";
+}
+
+const char* remoe_last_error(void) { return g_err.c_str(); }
+
+remoe_status_t remoe_nccl_unique_id(uint8_t out[128]) {
+  if (!out) return fail(REMOE_ERR_INVALID_ARG, "out is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  std::memcpy(out, &id, 128);
+  return REMOE_OK;
+}
+
+static remoe_status_t check_config(const remoe_sps_config_t* c) {
+  if (!c) return fail(REMOE_ERR_INVALID_ARG, "cfg is NULL");
+  if (c->n_local < 1) return fail(REMOE_ERR_INVALID_ARG, "n_local must be >= 1");
+  if (c->global_offset < 0) return fail(REMOE_ERR_INVALID_ARG, "global_offset must be >= 0");
+  if (c->global_offset + c->n_local > 0xFFFFFFFELL)
+    return fail(REMOE_ERR_UNSUPPORTED, "global ids must fit 32 bits");
+  if (c->dim < 8 || c->dim % 8 != 0) return fail(REMOE_ERR_INVALID_ARG, "dim must be a positive multiple of 8");
+  if (c->dim > 4096) return fail(REMOE_ERR_UNSUPPORTED, "dim > 4096");
+  if (c->n_layers < 1) return fail(REMOE_ERR_INVALID_ARG, "n_layers must be >= 1");
+  if (c->n_experts < 1) return fail(REMOE_ERR_INVALID_ARG, "n_experts must be >= 1");
+  if (c->n_experts > 256) return fail(REMOE_ERR_UNSUPPORTED, "n_experts > 256");
+  if (!(c->sigma > 0.f)) return fail(REMOE_ERR_INVALID_ARG, "sigma must be > 0 (Eq. 11)");
+  if (!(c->temperature > 0.f)) return fail(REMOE_ERR_INVALID_ARG, "temperature must be > 0");
+  if (c->max_batch < 1) return fail(REMOE_ERR_INVALID_ARG, "max_batch must be >= 1");
+  if (c->max_k < 1) return fail(REMOE_ERR_INVALID_ARG, "max_k must be >= 1");
+  if (c->max_k > 256) return fail(REMOE_ERR_UNSUPPORTED, "max_k > 256");
+  if (c->world < 1 || c->rank < 0 || c->rank >= c->world)
+    return fail(REMOE_ERR_INVALID_ARG, "need 0 <= rank < world");
+  if ((c->world == 1) != (c->nccl_unique_id == nullptr))
+    return fail(REMOE_ERR_INVALID_ARG, "nccl_unique_id must be NULL iff world == 1");
+  return REMOE_OK;
+}
+
+static remoe_status_t build_impl(remoe_sps* h, const uint16_t* emb, const float* act) {
+  const remoe_sps_config_t& c = h->cfg;
+  CUDA_TRY(cudaSetDevice(c.device));
+  CUDA_TRY(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, c.device));
+  h->LE = (int64_t)c.n_layers * c.n_experts;
+  cudaStream_t st = nullptr;
+  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamDestroy(s); } } sg{st};
+
+  // ---- bootstrap + shard tiling check
+  if (c.world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, c.nccl_unique_id, sizeof id);
+    NCCL_TRY(ncclCommInitRank(&h->comm, c.world, id, c.rank));
+    int64_t* d = nullptr;
+    ST_TRY(h->alloc((void**)&d, sizeof(int64_t) * 2 * (c.world + 1)));
+    int64_t mine[2] = {c.global_offset, c.n_local};
+    CUDA_TRY(cudaMemcpyAsync(d, mine, sizeof mine, cudaMemcpyHostToDevice, st));
+    NCCL_TRY(ncclAllGather(d, d + 2, 2, ncclInt64, h->comm, st));
+    std::vector<int64_t> all(2 * c.world);
+    CUDA_TRY(cudaMemcpyAsync(all.data(), d + 2, sizeof(int64_t) * 2 * c.world, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    int64_t expect = 0;
+    for (int g = 0; g < c.world; ++g) {
+      if (all[2 * g] != expect)
+        return fail(REMOE_ERR_INVALID_ARG, "shards do not tile [0, N): rank %d offset %lld, expected %lld",
+                    g, (long long)all[2 * g], (long long)expect);
+      expect += all[2 * g + 1];
+    }
+    h->n_total = expect;
+  } else {
+    h->n_total = c.n_local;
+  }
+
+  // ---- store
+  const size_t xbytes = (size_t)c.n_local * c.dim * 2;
+  const size_t abytes = (size_t)c.n_local * h->LE * 4;
+  ST_TRY(h->alloc((void**)&h->x, xbytes));
+  ST_TRY(h->alloc((void**)&h->xnorm, (size_t)c.n_local * 4));
+  ST_TRY(h->alloc((void**)&h->act, abytes));
+  const cudaMemcpyKind kind = c.inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  CUDA_TRY(cudaMemcpyAsync(h->x, emb, xbytes, kind, st));
+  CUDA_TRY(cudaMemcpyAsync(h->act, act, abytes, kind, st));
+  CUDA_TRY(remoe::launch_norms(h->x, c.n_local, c.dim, h->xnorm, st));
+  if (c.validate) {
+    unsigned long long* bad = nullptr;
+    ST_TRY(h->alloc((void**)&bad, 8));
+    CUDA_TRY(cudaMemsetAsync(bad, 0, 8, st));
+    CUDA_TRY(remoe::launch_validate(h->x, c.n_local, c.dim, h->act, c.n_local * c.n_layers,
+                                    c.n_experts, bad, st));
+    unsigned long long hb = 0;
+    CUDA_TRY(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (hb) return fail(REMOE_ERR_INVALID_ARG, "validate: %llu non-finite embeddings or invalid activation rows", hb);
+  }
+
+  // ---- kernel geometry + workspaces
+  h->grid_simt = h->num_sms;
+  h->stage_rows = std::max(1, std::min(64, 32768 / (2 * c.dim)));
+  const int capmax = 32 * remoe::topk_P(c.max_k);
+  ST_TRY(remoe::tc_plan_create(&h->tc, h->x, c.n_local, c.dim, h->num_sms, c.max_k));
+  h->grid_tc = h->tc.grid;
+  const int grid_max = std::max(h->grid_simt, h->grid_tc);
+  const int lanes_max = std::max(32, h->tc.threads_per_cta_queries);
+  const int mb = c.max_batch;
+  ST_TRY(h->alloc((void**)&h->qnorm, (size_t)mb * 4));
+  ST_TRY(h->alloc((void**)&h->cand_buf, (size_t)grid_max * lanes_max * capmax * 8));
+  ST_TRY(h->alloc((void**)&h->lists, (size_t)mb * grid_max * c.max_k * 8));
+  ST_TRY(h->alloc((void**)&h->local_top, (size_t)mb * c.max_k * 8));
+  ST_TRY(h->alloc((void**)&h->global_top, (size_t)mb * c.max_k * 8));
+  if (c.world > 1) {
+    ST_TRY(h->alloc((void**)&h->gathered, (size_t)c.world * mb * c.max_k * 8));
+    ST_TRY(h->alloc((void**)&h->rows, (size_t)mb * c.max_k * h->LE * 4));
+  }
+  ST_TRY(h->alloc((void**)&h->hq, (size_t)mb * c.dim * 2));
+  ST_TRY(h->alloc((void**)&h->hids, (size_t)mb * c.max_k * 8));
+  ST_TRY(h->alloc((void**)&h->hscores, (size_t)mb * c.max_k * 4));
+  ST_TRY(h->alloc((void**)&h->hpred, (size_t)mb * h->LE * 4));
+  CUDA_TRY(cudaStreamSynchronize(st));
+
+  if (const char* f = getenv("REMOE_FORCE_KERNEL")) {
+    if (!strcmp(f, "stream")) h->force_kernel = 1;
+    else if (!strcmp(f, "tc")) h->force_kernel = 2;
+  }
+  return REMOE_OK;
+}
+
+remoe_status_t remoe_sps_build(const remoe_sps_config_t* cfg, const uint16_t* emb_bf16,
+                               const float* act, remoe_sps_t* out) {
+  if (!out) return fail(REMOE_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  ST_TRY(check_config(cfg));
+  if (!emb_bf16 || !act) return fail(REMOE_ERR_INVALID_ARG, "emb/act is NULL");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(REMOE_ERR_CUDA, "no CUDA device visible");
+  if (cfg->device < 0 || cfg->device >= ndev) return fail(REMOE_ERR_INVALID_ARG, "device out of range");
+  remoe_sps* h = new (std::nothrow) remoe_sps();
+  if (!h) return fail(REMOE_ERR_OOM, "host allocation failed");
+  h->cfg = *cfg;
+  DeviceGuard dg(cfg->device);
+  remoe_status_t s = build_impl(h, emb_bf16, act);
+  h->cfg.nccl_unique_id = nullptr;  // the caller owns those bytes; not kept past build
+  if (s == REMOE_OK) {
+    *out = h;
+  } else {
+    h->release();
+    delete h;
+  }
+  return s;
+}
+
+static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k, int64_t* ids,
+                                  float* scores, float* pred, cudaStream_t st, int* launches) {
+  const remoe_sps_config_t& c = h->cfg;
+  CUDA_TRY(remoe::launch_norms(q, bc, c.dim, h->qnorm, st));
+  ++*launches;
+  // ---- S2+S3
+  int which = h->force_kernel;
+  if (which == 0) which = (bc <= remoe::kSimtMaxB || !h->tc.ok) ? 1 : 2;
+  if (which == 2 && !h->tc.ok) return fail(REMOE_ERR_UNSUPPORTED, "tensor-core scan unavailable: %s", h->tc.why);
+  int grid = 0;
+  CUDA_TRY(h->prof_mark(st, true));
+  if (which == 1) {
+    grid = h->grid_simt;
+    const int BQ = bc >= 8 ? 8 : bc >= 4 ? 4 : bc >= 2 ? 2 : 1;
+    const int NST = std::max(2, std::min(6, (int)((200 * 1024 - (size_t)BQ * c.dim * 4) /
+                                                   ((size_t)h->stage_rows * c.dim * 2))));
+    for (int s0 = 0; s0 < bc; s0 += BQ) {
+      remoe::SimtScanParams p{};
+      p.x = h->x; p.xnorm = h->xnorm; p.n_rows = c.n_local; p.gid_offset = c.global_offset;
+      p.dim = c.dim; p.q = q + (size_t)s0 * c.dim; p.qnorm = h->qnorm + s0;
+      p.nq = std::min(BQ, bc - s0); p.k = k; p.sigma = c.sigma;
+      p.stage_rows = h->stage_rows; p.n_stages_ring = NST;
+      p.cand_buf = h->cand_buf; p.out = h->lists + (size_t)s0 * grid * k;
+      CUDA_TRY(remoe::launch_scan_simt(p, BQ, grid, st));
+      ++*launches;
+      ++h->prof_launches;
+    }
+  } else {
+    grid = h->grid_tc;
+    int nl = 0;
+    ST_TRY(remoe::tc_scan(&h->tc, q, h->qnorm, bc, k, c.sigma, h->xnorm, c.n_local, c.global_offset,
+                          h->cand_buf, h->lists, st, &nl));
+    *launches += nl;
+    h->prof_launches += nl;
+  }
+  CUDA_TRY(h->prof_mark(st, false));
+  h->last_kernel = which;
+  // ---- S4
+  uint64_t* top = h->local_top;
+  CUDA_TRY(remoe::launch_merge(h->lists, bc, grid, (int64_t)grid * k, k, k, h->local_top, st));
+  ++*launches;
+  // ---- S5
+  if (c.world > 1) {
+    NCCL_TRY(ncclAllGather(h->local_top, h->gathered, (size_t)bc * k, ncclUint64, h->comm, st));
+    CUDA_TRY(remoe::launch_merge(h->gathered, bc, c.world, k, (int64_t)bc * k, k, h->global_top, st));
+    ++*launches;
+    top = h->global_top;
+  }
+  // ---- S6 + S7
+  if (pred && c.world > 1) {
+    CUDA_TRY(remoe::launch_gather_rows(top, bc, k, h->act, c.global_offset, c.n_local, h->LE, h->rows, st));
+    NCCL_TRY(ncclAllReduce(h->rows, h->rows, (size_t)bc * k * h->LE, ncclFloat, ncclSum, h->comm, st));
+    CUDA_TRY(remoe::launch_finalize(top, bc, k, h->act, c.global_offset, h->rows, 1, h->LE,
+                                    c.temperature, ids, scores, pred, st));
+    *launches += 2;
+  } else {
+    CUDA_TRY(remoe::launch_finalize(top, bc, k, h->act, c.global_offset, nullptr, 0, h->LE,
+                                    c.temperature, ids, scores, pred, st));
+    ++*launches;
+  }
+  return REMOE_OK;
+}
+
+static remoe_status_t check_query(remoe_sps* h, const uint16_t* q, int32_t B, int32_t k,
+                                  const int64_t* ids, const float* scores) {
+  if (!h) return fail(REMOE_ERR_STATE, "handle is NULL");
+  if (B < 0) return fail(REMOE_ERR_INVALID_ARG, "B must be >= 0");
+  if (k < 1) return fail(REMOE_ERR_INVALID_ARG, "k must be >= 1");
+  if (k > h->cfg.max_k) return fail(REMOE_ERR_INVALID_ARG, "k=%d exceeds max_k=%d", k, h->cfg.max_k);
+  if (k > h->n_total)
+    return fail(REMOE_ERR_INVALID_ARG, "k=%d exceeds the history size %lld (SPEC S:227)", k,
+                (long long)h->n_total);
+  if (B > 0 && (!q || !ids || !scores)) return fail(REMOE_ERR_INVALID_ARG, "q/ids/scores is NULL");
+  return REMOE_OK;
+}
+
+remoe_status_t remoe_sps_query(remoe_sps_t h, const uint16_t* q, int32_t B, int32_t k,
+                               int64_t* ids, float* scores, float* pred, void* stream) {
+  ST_TRY(check_query(h, q, B, k, ids, scores));
+  if (B == 0) return REMOE_OK;
+  DeviceGuard dg(h->cfg.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  int launches = 0;
+  const int mb = h->cfg.max_batch;
+  for (int b0 = 0; b0 < B; b0 += mb) {
+    const int bc = std::min(mb, B - b0);
+    ST_TRY(query_chunk(h, q + (size_t)b0 * h->cfg.dim, bc, k, ids + (size_t)b0 * k,
+                       scores + (size_t)b0 * k, pred ? pred + (size_t)b0 * h->LE : nullptr, st,
+                       &launches));
+  }
+  h->last_launches = launches;
+  return REMOE_OK;
+}
+
+remoe_status_t remoe_sps_query_host(remoe_sps_t h, const uint16_t* q, int32_t B, int32_t k,
+                                    int64_t* ids, float* scores, float* pred, void* stream) {
+  ST_TRY(check_query(h, q, B, k, ids, scores));
+  if (B == 0) return REMOE_OK;
+  DeviceGuard dg(h->cfg.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int mb = h->cfg.max_batch;
+  const int D = h->cfg.dim;
+  int launches = 0;
+  for (int b0 = 0; b0 < B; b0 += mb) {
+    const int bc = std::min(mb, B - b0);
+    CUDA_TRY(cudaMemcpyAsync(h->hq, q + (size_t)b0 * D, (size_t)bc * D * 2, cudaMemcpyHostToDevice, st));
+    ST_TRY(query_chunk(h, h->hq, bc, k, h->hids, h->hscores, pred ? h->hpred : nullptr, st, &launches));
+    CUDA_TRY(cudaMemcpyAsync(ids + (size_t)b0 * k, h->hids, (size_t)bc * k * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(scores + (size_t)b0 * k, h->hscores, (size_t)bc * k * 4, cudaMemcpyDeviceToHost, st));
+    if (pred)
+      CUDA_TRY(cudaMemcpyAsync(pred + (size_t)b0 * h->LE, h->hpred, (size_t)bc * h->LE * 4,
+                               cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  h->last_launches = launches;
+  return REMOE_OK;
+}
+
+remoe_status_t remoe_expert_plan(const float* pred, int32_t B, int32_t L, int32_t E, int32_t n_cold,
+                                 uint8_t* cold_mask, void* stream) {
+  if (B < 0 || L < 1 || E < 1) return fail(REMOE_ERR_INVALID_ARG, "need B >= 0, L >= 1, E >= 1");
+  if (E > 256) return fail(REMOE_ERR_UNSUPPORTED, "E > 256");
+  if (n_cold < 0 || n_cold > E) return fail(REMOE_ERR_INVALID_ARG, "need 0 <= n_cold <= E");
+  if (B == 0) return REMOE_OK;
+  if (!pred || !cold_mask) return fail(REMOE_ERR_INVALID_ARG, "pred/cold_mask is NULL");
+  CUDA_TRY(remoe::launch_plan(pred, B, L, E, n_cold, cold_mask, (cudaStream_t)stream));
+  return REMOE_OK;
+}
+
+remoe_status_t remoe_sps_sync(remoe_sps_t h) {
+  if (!h) return fail(REMOE_ERR_STATE, "handle is NULL");
+  DeviceGuard dg(h->cfg.device);
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaGetLastError());
+  if (h->comm) {
+    ncclResult_t ar = ncclSuccess;
+    NCCL_TRY(ncclCommGetAsyncError(h->comm, &ar));
+    if (ar != ncclSuccess) return fail(REMOE_ERR_NCCL, "async NCCL error: %s", ncclGetErrorString(ar));
+  }
+  return REMOE_OK;
+}
+
+remoe_status_t remoe_sps_get_info(remoe_sps_t h, remoe_sps_info_t* info) {
+  if (!h) return fail(REMOE_ERR_STATE, "handle is NULL");
+  if (!info) return fail(REMOE_ERR_INVALID_ARG, "info is NULL");
+  info->n_total = h->n_total;
+  info->n_local = h->cfg.n_local;
+  info->global_offset = h->cfg.global_offset;
+  info->dim = h->cfg.dim;
+  info->n_layers = h->cfg.n_layers;
+  info->n_experts = h->cfg.n_experts;
+  info->rank = h->cfg.rank;
+  info->world = h->cfg.world;
+  info->last_scan_kernel = h->last_kernel;
+  info->last_launches = h->last_launches;
+  info->scan_ctas = h->last_kernel == 2 ? h->grid_tc : h->grid_simt;
+  info->device_bytes = (int64_t)h->device_bytes;
+  return REMOE_OK;
+}
+
+remoe_status_t remoe_sps_set_kernel(remoe_sps_t h, int32_t which) {
+  if (!h) return fail(REMOE_ERR_STATE, "handle is NULL");
+  if (which < 0 || which > 2) return fail(REMOE_ERR_INVALID_ARG, "which must be 0, 1 or 2");
+  if (which == 2 && !h->tc.ok) return fail(REMOE_ERR_UNSUPPORTED, "tensor-core scan unavailable: %s", h->tc.why);
+  h->force_kernel = which;
+  return REMOE_OK;
+}
+
+remoe_status_t remoe_sps_profile(remoe_sps_t h, int32_t enable, double* scan_ms, int64_t* launches) {
+  if (!h) return fail(REMOE_ERR_STATE, "handle is NULL");
+  DeviceGuard dg(h->cfg.device);
+  CUDA_TRY(h->prof_collect());
+  if (scan_ms) *scan_ms = h->prof_ms;
+  if (launches) *launches = h->prof_launches;
+  h->prof_ms = 0.0;
+  h->prof_launches = 0;
+  h->prof = enable != 0;
+  return REMOE_OK;
+}
+
+void remoe_sps_destroy(remoe_sps_t h) {
+  if (!h) return;
+  {
+    DeviceGuard dg(h->cfg.device);
+    cudaDeviceSynchronize();
+    h->release();
+  }
+  delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,273 @@
+"""Thin ctypes binding of include/remoe.h (argument marshalling only).
+
+Every step of the SPS path runs in libremoe.so's CUDA kernels; this module only
+turns torch tensors / numpy arrays into pointers, picks the current CUDA stream,
+and raises on non-OK status.  There is no CPU fallback: if libremoe.so is
+missing or no GPU is visible, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libremoe.so")
+
+REMOE_OK = 0
+STATUS = {0: "OK", 1: "INVALID_ARG", 2: "CUDA", 3: "NCCL", 4: "OOM", 5: "UNSUPPORTED", 6: "STATE"}
+KERNEL_AUTO, KERNEL_STREAM, KERNEL_TC = 0, 1, 2
+
+# every function declared in include/remoe.h
+ABI_FUNCTIONS = (
+    "remoe_sps_config_default", "remoe_sps_build", "remoe_sps_query", "remoe_sps_query_host",
+    "remoe_expert_plan", "remoe_nccl_unique_id", "remoe_sps_sync", "remoe_sps_get_info",
+    "remoe_sps_set_kernel", "remoe_sps_profile", "remoe_sps_destroy", "remoe_status_string",
+    "remoe_last_error",
+)
+
+
+class RemoeError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class SpsConfig(ctypes.Structure):
+    _fields_ = [
+        ("n_local", ctypes.c_int64),
+        ("global_offset", ctypes.c_int64),
+        ("dim", ctypes.c_int32),
+        ("n_layers", ctypes.c_int32),
+        ("n_experts", ctypes.c_int32),
+        ("sigma", ctypes.c_float),
+        ("temperature", ctypes.c_float),
+        ("max_batch", ctypes.c_int32),
+        ("max_k", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("world", ctypes.c_int32),
+        ("nccl_unique_id", ctypes.c_void_p),
+        ("inputs_on_device", ctypes.c_int32),
+        ("validate", ctypes.c_int32),
+    ]
+
+
+class SpsInfo(ctypes.Structure):
+    _fields_ = [
+        ("n_total", ctypes.c_int64),
+        ("n_local", ctypes.c_int64),
+        ("global_offset", ctypes.c_int64),
+        ("dim", ctypes.c_int32),
+        ("n_layers", ctypes.c_int32),
+        ("n_experts", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("world", ctypes.c_int32),
+        ("last_scan_kernel", ctypes.c_int32),
+        ("last_launches", ctypes.c_int32),
+        ("scan_ctas", ctypes.c_int32),
+        ("device_bytes", ctypes.c_int64),
+    ]
+
+
+_LIB = None
+
+
+def lib():
+    """Load libremoe.so (raises if it was not built)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with `make` or "
+                               "__graft_entry__.build(); there is no fallback path")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        L.remoe_sps_config_default.argtypes = [ctypes.POINTER(SpsConfig)]
+        L.remoe_sps_config_default.restype = None
+        L.remoe_sps_build.argtypes = [ctypes.POINTER(SpsConfig), vp, vp, ctypes.POINTER(vp)]
+        L.remoe_sps_query.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp]
+        L.remoe_sps_query_host.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp]
+        L.remoe_expert_plan.argtypes = [vp, i32, i32, i32, i32, vp, vp]
+        L.remoe_nccl_unique_id.argtypes = [vp]
+        L.remoe_sps_sync.argtypes = [vp]
+        L.remoe_sps_get_info.argtypes = [vp, ctypes.POINTER(SpsInfo)]
+        L.remoe_sps_set_kernel.argtypes = [vp, i32]
+        L.remoe_sps_profile.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_double),
+                                        ctypes.POINTER(ctypes.c_int64)]
+        L.remoe_sps_destroy.argtypes = [vp]
+        L.remoe_sps_destroy.restype = None
+        L.remoe_status_string.argtypes = [i32]
+        L.remoe_status_string.restype = ctypes.c_char_p
+        L.remoe_last_error.argtypes = []
+        L.remoe_last_error.restype = ctypes.c_char_p
+        for f in ("remoe_sps_build", "remoe_sps_query", "remoe_sps_query_host", "remoe_expert_plan",
+                  "remoe_nccl_unique_id", "remoe_sps_sync", "remoe_sps_get_info",
+                  "remoe_sps_set_kernel", "remoe_sps_profile"):
+            getattr(L, f).restype = i32
+        _LIB = L
+    return _LIB
+
+
+def _check(status: int):
+    if status != REMOE_OK:
+        raise RemoeError(status, lib().remoe_last_error().decode(errors="replace"))
+
+
+def _ptr(t) -> int | None:
+    """Raw pointer of a torch tensor or numpy array (None passes through)."""
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        assert t.flags.c_contiguous, "array must be C-contiguous"
+        return t.ctypes.data
+    assert t.is_contiguous(), "tensor must be contiguous"
+    return t.data_ptr()
+
+
+def _stream(stream) -> int | None:
+    if stream is not None:
+        return int(stream) if isinstance(stream, int) else stream.cuda_stream
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
+# ------------------------------------------------------------------ C-ABI-named calls
+
+def remoe_sps_config_default() -> SpsConfig:
+    c = SpsConfig()
+    lib().remoe_sps_config_default(ctypes.byref(c))
+    return c
+
+
+def remoe_nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().remoe_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def remoe_sps_build(cfg: SpsConfig, emb_bf16, act, nccl_unique_id: bytes | None = None) -> int:
+    """S0.  emb_bf16: uint16/int16/bfloat16 [n_local, D]; act: float32 [n_local, L, E]."""
+    idbuf = None
+    if nccl_unique_id is not None:
+        idbuf = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_unique_id)
+        cfg.nccl_unique_id = ctypes.cast(idbuf, ctypes.c_void_p)
+    h = ctypes.c_void_p()
+    _check(lib().remoe_sps_build(ctypes.byref(cfg), _ptr(emb_bf16), _ptr(act), ctypes.byref(h)))
+    cfg.nccl_unique_id = None
+    return h.value
+
+
+def remoe_sps_query(h: int, q_bf16, B: int, k: int, ids, scores, pred=None, stream=None):
+    """S1-S7 on device buffers (torch CUDA tensors)."""
+    _check(lib().remoe_sps_query(h, _ptr(q_bf16), B, k, _ptr(ids), _ptr(scores), _ptr(pred),
+                                 _stream(stream)))
+
+
+def remoe_sps_query_host(h: int, q_bf16, B: int, k: int, ids, scores, pred=None, stream=None):
+    """S1-S7 on host buffers (numpy or pinned CPU tensors); synchronous."""
+    _check(lib().remoe_sps_query_host(h, _ptr(q_bf16), B, k, _ptr(ids), _ptr(scores), _ptr(pred),
+                                      _stream(stream)))
+
+
+def remoe_expert_plan(pred, B: int, L: int, E: int, n_cold: int, cold_mask, stream=None):
+    """S8 on device buffers."""
+    _check(lib().remoe_expert_plan(_ptr(pred), B, L, E, n_cold, _ptr(cold_mask), _stream(stream)))
+
+
+def remoe_sps_sync(h: int):
+    _check(lib().remoe_sps_sync(h))
+
+
+def remoe_sps_get_info(h: int) -> SpsInfo:
+    info = SpsInfo()
+    _check(lib().remoe_sps_get_info(h, ctypes.byref(info)))
+    return info
+
+
+def remoe_sps_set_kernel(h: int, which: int):
+    _check(lib().remoe_sps_set_kernel(h, which))
+
+
+def remoe_sps_profile(h: int, enable: bool) -> tuple[float, int]:
+    """Scan-kernel time (ms) and launches since the previous call; toggles recording."""
+    ms = ctypes.c_double()
+    n = ctypes.c_int64()
+    _check(lib().remoe_sps_profile(h, 1 if enable else 0, ctypes.byref(ms), ctypes.byref(n)))
+    return ms.value, n.value
+
+
+def remoe_sps_destroy(h: int):
+    if h:
+        lib().remoe_sps_destroy(h)
+
+
+# ------------------------------------------------------------------ convenience wrapper
+
+class Sps:
+    """Owns one handle.  Tensors in, tensors out (torch on the handle's device)."""
+
+    def __init__(self, emb_bf16, act, *, sigma=1e-6, temperature=1.0, max_batch=256, max_k=128,
+                 device=0, rank=0, world=1, global_offset=0, nccl_unique_id=None, validate=True):
+        import torch
+        cfg = remoe_sps_config_default()
+        n, d = emb_bf16.shape
+        cfg.n_local, cfg.global_offset, cfg.dim = n, global_offset, d
+        cfg.n_layers, cfg.n_experts = act.shape[1], act.shape[2]
+        cfg.sigma, cfg.temperature = sigma, temperature
+        cfg.max_batch, cfg.max_k = max_batch, max_k
+        cfg.device, cfg.rank, cfg.world = device, rank, world
+        cfg.validate = 1 if validate else 0
+        on_dev = isinstance(emb_bf16, torch.Tensor) and emb_bf16.is_cuda
+        cfg.inputs_on_device = 1 if on_dev else 0
+        self.device = torch.device("cuda", device)
+        self.dim, self.layers, self.experts = d, act.shape[1], act.shape[2]
+        self.handle = remoe_sps_build(cfg, emb_bf16, act, nccl_unique_id)
+
+    def query(self, q_bf16, k, want_pred=True, stream=None):
+        import torch
+        B = q_bf16.shape[0]
+        ids = torch.empty((B, k), dtype=torch.int64, device=self.device)
+        scores = torch.empty((B, k), dtype=torch.float32, device=self.device)
+        pred = (torch.empty((B, self.layers, self.experts), dtype=torch.float32, device=self.device)
+                if want_pred else None)
+        remoe_sps_query(self.handle, q_bf16, B, k, ids, scores, pred, stream)
+        return ids, scores, pred
+
+    def query_host(self, q_bf16: np.ndarray, k: int, want_pred=True, stream=None):
+        B = q_bf16.shape[0]
+        ids = np.empty((B, k), np.int64)
+        scores = np.empty((B, k), np.float32)
+        pred = np.empty((B, self.layers, self.experts), np.float32) if want_pred else None
+        remoe_sps_query_host(self.handle, q_bf16, B, k, ids, scores, pred, stream)
+        return ids, scores, pred
+
+    def plan(self, pred, n_cold, stream=None):
+        import torch
+        B, L, E = pred.shape
+        mask = torch.empty((B, L, E), dtype=torch.uint8, device=pred.device)
+        remoe_expert_plan(pred, B, L, E, n_cold, mask, stream)
+        return mask
+
+    def set_kernel(self, which: int):
+        remoe_sps_set_kernel(self.handle, which)
+
+    def info(self) -> SpsInfo:
+        return remoe_sps_get_info(self.handle)
+
+    def profile(self, enable: bool) -> tuple[float, int]:
+        return remoe_sps_profile(self.handle, enable)
+
+    def sync(self):
+        remoe_sps_sync(self.handle)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            remoe_sps_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

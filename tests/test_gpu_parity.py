@@ -1,0 +1,297 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by element.
+
+Sizes the oracle finishes in seconds that still span several tiles / CTAs and a
+ragged tail, plus sampled queries at BASELINE's full c3 size in the launch
+configuration bench.py times.  Protocol: tests/parity.py.
+"""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from parity import compare, plan_compare
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("remoe_lib_built")]
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU box
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2512_18674_b200 as remoe  # noqa: E402
+
+KERNELS = {"stream": remoe.KERNEL_STREAM, "tc": remoe.KERNEL_TC}
+
+
+def _store(name, n=None):
+    c = gen.CONFIGS[name]
+    n = n or c.n
+    x = gen.store_emb(c.store_seed, n, c.dim)
+    a = gen.store_act(c.store_seed, n, c.layers, c.experts, c.moe_topk)
+    return c, x, a
+
+
+_CACHE = {}
+
+
+def store(name, n=None):
+    key = (name, n)
+    if key not in _CACHE:
+        _CACHE[key] = _store(name, n)
+    return _CACHE[key]
+
+
+def run(sps, q_bits, k, want_pred=True):
+    q = torch.from_numpy(q_bits.view(np.int16)).cuda()
+    ids, sc, pred = sps.query(q, k, want_pred)
+    torch.cuda.synchronize()
+    return (ids.cpu().numpy(), sc.cpu().numpy(), pred.cpu().numpy() if want_pred else None)
+
+
+def make(x, a, **kw):
+    return remoe.Sps(x, a, **kw)
+
+
+def kernel_available(sps, which):
+    try:
+        sps.set_kernel(KERNELS[which])
+        return True
+    except remoe.RemoeError:
+        return False
+
+
+def assert_parity(rep):
+    assert rep.ok(), "\n".join(rep.failures[:20])
+
+
+# ------------------------------------------------------------------ tiny: everything, full
+
+@pytest.mark.parametrize("kern", ["stream", "tc"])
+def test_tiny_full(kern):
+    c, x, a = store("tiny")
+    q = gen.queries(c.store_seed, c.query_seed, c.n, c.dim, c.batch, mode=1)
+    s = make(x, a, max_k=32)
+    if not kernel_available(s, kern):
+        pytest.skip(f"{kern} kernel unavailable")
+    ids, sc, pred = run(s, q, c.k)
+    rep = compare(q, x, a, c.k, ids, sc, pred, exact_ids=True)
+    assert_parity(rep)
+    assert s.info().last_scan_kernel == KERNELS[kern]
+    # exact copies retrieve their source row first; duplicates are bit-identical
+    for i in range(c.batch):
+        if i % 8 in (4, 5):
+            assert ids[i, 0] == gen.query_source_row(c.query_seed, c.n, i)
+        if i % 8 == 7:
+            assert np.array_equal(ids[i], ids[i - 1]) and np.array_equal(pred[i], pred[i - 1])
+            assert np.array_equal(sc[i], sc[i - 1])
+
+
+# ------------------------------------------------------------------ c2: batch sweep
+
+_C2Q = {}
+
+
+def c2_oracle(B, k):
+    c, x, a = store("c2")
+    key = (B, k)
+    if key not in _C2Q:
+        q = gen.queries(c.store_seed, c.query_seed, c.n, c.dim, B, mode=1)
+        _C2Q[key] = (q, oracle.sps(q, x, a, k))
+    return _C2Q[key]
+
+
+@pytest.mark.parametrize("kern", ["stream", "tc"])
+@pytest.mark.parametrize("B", [1, 2, 3, 4, 8, 16, 64, 256])
+def test_c2_batch_sweep(kern, B):
+    c, x, a = store("c2")
+    q_all, o_all = c2_oracle(256, c.k)
+    q = q_all[:B]
+    o = tuple(v[:B] for v in o_all)
+    s = make(x, a, max_k=64)
+    if not kernel_available(s, kern):
+        pytest.skip(f"{kern} kernel unavailable")
+    if kern == "stream" and B > 16:
+        pytest.skip("streaming kernel is only used for small batches")
+    ids, sc, pred = run(s, q, c.k)
+    rep = compare(q, x, a, c.k, ids, sc, pred, oracle_out=o)
+    assert_parity(rep)
+    assert rep.substitutions == 0, "c2 is well separated at k=10: ids must match exactly"
+
+
+@pytest.mark.parametrize("kern", ["stream", "tc"])
+@pytest.mark.parametrize("k", [1, 2, 5, 16, 32, 64, 128, 256])
+def test_c2_k_sweep(kern, k):
+    c, x, a = store("c2", 20_000)
+    q = gen.queries(c.store_seed, c.query_seed, 20_000, c.dim, 8, mode=1)
+    s = make(x, a, max_k=256)
+    if not kernel_available(s, kern):
+        pytest.skip(f"{kern} kernel unavailable")
+    ids, sc, pred = run(s, q, k)
+    rep = compare(q, x, a, k, ids, sc, pred)
+    assert_parity(rep)
+
+
+# ------------------------------------------------------------------ invariants
+
+@pytest.mark.parametrize("kern", ["stream", "tc"])
+def test_invariants_rerun_batch_order_k1(kern):
+    c, x, a = store("c2", 30_000)
+    q = gen.queries(c.store_seed, c.query_seed, 30_000, c.dim, 24, mode=1)
+    s = make(x, a, max_k=32)
+    if not kernel_available(s, kern):
+        pytest.skip(f"{kern} kernel unavailable")
+    r1 = run(s, q, 10)
+    r2 = run(s, q, 10)
+    for u, v in zip(r1, r2):
+        assert np.array_equal(u, v), "reruns must be bit-identical"
+    perm = np.random.default_rng(0).permutation(24)
+    rp = run(s, q[perm], 10)
+    for u, v in zip(r1, rp):
+        assert np.array_equal(u[perm], v), "outputs must be invariant to batch order"
+    # k = 1: exact copies return their source with w = 1 -> pred == table row bit-exact
+    ids, sc, pred = run(s, q, 1)
+    for i in range(24):
+        if i % 8 in (4, 5):
+            src = gen.query_source_row(c.query_seed, 30_000, i)
+            assert ids[i, 0] == src
+            assert np.array_equal(pred[i], a[src])
+    # convex hull (+-1e-5) and per-layer row sums of the prediction
+    ids, sc, pred = r1
+    for i in range(24):
+        nb = a[ids[i]]
+        assert np.all(pred[i] >= nb.min(0) - 1e-5) and np.all(pred[i] <= nb.max(0) + 1e-5)
+        np.testing.assert_allclose(pred[i].sum(-1), 1.0, atol=2e-5)
+
+
+# ------------------------------------------------------------------ edge cases
+
+@pytest.mark.parametrize("kern", ["stream", "tc"])
+@pytest.mark.parametrize("n", [1, 2, 7, 64, 149, 300])
+def test_small_stores_k_equals_n(kern, n):
+    """Fewer rows than CTAs, k = N returns every row in key order."""
+    c, x, a = store("tiny")
+    x, a = x[:n].copy(), a[:n].copy()
+    q = gen.queries(c.store_seed, c.query_seed, c.n, c.dim, 5, mode=0)
+    s = make(x, a, max_k=256)
+    if not kernel_available(s, kern):
+        pytest.skip(f"{kern} kernel unavailable")
+    k = min(n, 256)
+    ids, sc, pred = run(s, q, k)
+    assert_parity(compare(q, x, a, k, ids, sc, pred))
+    for i in range(5):
+        assert sorted(ids[i].tolist()) == sorted(set(ids[i].tolist()))
+
+
+@pytest.mark.parametrize("kern", ["stream", "tc"])
+def test_degenerate_rows(kern):
+    """Zero rows score 0; exact duplicate rows tie and the lower id comes first;
+    a zero query scores 0 everywhere (sigma keeps it finite)."""
+    c, x, a = store("tiny")
+    x = x[:500].copy()
+    a = a[:500].copy()
+    x[3] = 0
+    x[100] = x[50]
+    x[400] = x[50]
+    q = np.stack([x[50], np.zeros_like(x[0]), x[7]])
+    s = make(x, a, max_k=16)
+    if not kernel_available(s, kern):
+        pytest.skip(f"{kern} kernel unavailable")
+    ids, sc, pred = run(s, q, 5)
+    assert list(ids[0, :3]) == [50, 100, 400] and sc[0, 0] == sc[0, 1] == sc[0, 2]
+    assert np.all(sc[1] == 0.0) and list(ids[1]) == [0, 1, 2, 3, 4]
+    assert_parity(compare(q, x, a, 5, ids, sc, pred))
+
+
+def test_dims_and_table_shapes():
+    """D at the minimum (8), odd chunk counts (D=40, 776), D=4096, E=1 and E=256."""
+    rng = np.random.default_rng(4)
+    for D, L, E, n in [(8, 3, 1, 777), (40, 2, 256, 3000), (776, 27, 64, 5000), (4096, 4, 8, 2000)]:
+        x = gen.f32_to_bf16_bits(rng.standard_normal((n, D)).astype(np.float32))
+        a = rng.random((n, L, E)).astype(np.float32) + 1e-3
+        a /= a.sum(-1, keepdims=True)
+        q = gen.f32_to_bf16_bits(rng.standard_normal((6, D)).astype(np.float32))
+        s = make(x, a, max_k=32)
+        for kern in ("stream", "tc"):
+            if not kernel_available(s, kern):
+                continue
+            ids, sc, pred = run(s, q, 9)
+            assert_parity(compare(q, x, a, 9, ids, sc, pred))
+        s.close()
+
+
+def test_chunking_above_max_batch():
+    c, x, a = store("c2", 20_000)
+    q = gen.queries(c.store_seed, c.query_seed, 20_000, c.dim, 37, mode=1)
+    s = make(x, a, max_batch=5, max_k=16)
+    ids, sc, pred = run(s, q, 10)
+    assert_parity(compare(q, x, a, 10, ids, sc, pred))
+
+
+def test_errors():
+    c, x, a = store("tiny")
+    s = make(x, a, max_k=8)
+    q = torch.zeros((2, c.dim), dtype=torch.int16, device="cuda")
+    with pytest.raises(remoe.RemoeError, match="INVALID_ARG"):
+        s.query(q, 9)          # k > max_k
+    with pytest.raises(remoe.RemoeError, match="INVALID_ARG"):
+        s.query(q, 0)
+    s2 = make(x[:4].copy(), a[:4].copy(), max_k=8)
+    with pytest.raises(remoe.RemoeError, match="INVALID_ARG"):
+        s2.query(q, 5)         # k > N
+    ids, sc, pred = s.query(q[:0], 3)  # B == 0: no-op
+    assert ids.shape == (0, 3)
+    bad = x.copy()
+    bad[5, 3] = 0x7FC0       # NaN
+    with pytest.raises(remoe.RemoeError, match="INVALID_ARG"):
+        make(bad, a)
+    bada = a.copy()
+    bada[9, 1, 0] += 0.5     # row no longer sums to 1
+    with pytest.raises(remoe.RemoeError, match="INVALID_ARG"):
+        make(x, bada)
+    with pytest.raises(remoe.RemoeError, match="UNSUPPORTED"):
+        make(x, a, max_k=300)
+
+
+def test_host_path_matches_device_path():
+    c, x, a = store("c2", 20_000)
+    q = gen.queries(c.store_seed, c.query_seed, 20_000, c.dim, 12, mode=1)
+    s = make(x, a, max_batch=8, max_k=16)
+    d = run(s, q, 10)
+    h = s.query_host(q, 10)
+    for u, v in zip(d, h):
+        assert np.array_equal(u, v)
+
+
+# ------------------------------------------------------------------ S8 expert plan
+
+def test_expert_plan_vs_oracle():
+    c, x, a = store("c2", 20_000)
+    q = gen.queries(c.store_seed, c.query_seed, 20_000, c.dim, 16, mode=1)
+    s = make(x, a, max_k=16)
+    ids, sc, pred = run(s, q, 10)
+    pt = torch.from_numpy(pred).cuda()
+    for n_cold in (0, 1, 13, 32, 63, 64):
+        m = s.plan(pt, n_cold).cpu().numpy()
+        assert not plan_compare(pred.astype(np.float64), m, n_cold)
+        assert np.all(m.sum(-1) == n_cold)
+    # SPEC S:434 worked example, and ties -> lower index goes cold first
+    p = torch.tensor([[[0.4, 0.3, 0.2, 0.1]], [[0.25, 0.25, 0.25, 0.25]]], device="cuda")
+    m = s.plan(p, 2).cpu().numpy()
+    assert list(m[0, 0]) == [0, 0, 1, 1] and list(m[1, 0]) == [1, 1, 0, 0]
+
+
+# ------------------------------------------------------------------ full-size sampled parity
+
+@pytest.mark.parametrize("kern", ["stream", "tc"])
+def test_c3_full_size_sampled(kern):
+    """BASELINE c3 (1M x 1024, 24x60, k=16) at its bench batch B=64 (and B=4 for the
+    streaming kernel); 6 sampled queries checked against the oracle one by one."""
+    c, x, a = store("c3")
+    B = 64 if kern == "tc" else 4
+    q = gen.queries(c.store_seed, c.query_seed, c.n, c.dim, B, mode=1)
+    s = make(x, a, max_k=c.k, max_batch=256)
+    if not kernel_available(s, kern):
+        pytest.skip(f"{kern} kernel unavailable")
+    ids, sc, pred = run(s, q, c.k)
+    pick = sorted({0, 1, 3, min(B - 1, 4), min(B - 1, 6), B - 1})
+    rep = compare(q[pick], x, a, c.k, ids[pick], sc[pick], pred[pick])
+    assert_parity(rep)
