@@ -117,29 +117,86 @@ __device__ __forceinline__ uint64_t warp_compact(uint64_t* buf, int cnt, int k, 
   return cnt >= k ? warp_key_at<P>(v, k - 1) : 0ull;
 }
 
+// Slow path of LaneTopk::push (rare, kept out of line): compact the full buffer of
+// every lane named in `full` (warp-uniform); returns this lane's new threshold.
+template <int P>
+__device__ __noinline__ uint64_t lane_compact_slow(unsigned full, uint64_t* mybuf, int k) {
+  const int lane = threadIdx.x & 31;
+  uint64_t mine = 0;
+  while (full) {
+    const int L = __ffs(full) - 1;
+    full &= full - 1;
+    uint64_t* b = (uint64_t*)__shfl_sync(kFull, (unsigned long long)mybuf, L);
+    const uint64_t t = warp_compact<P>(b, 32 * P, k, nullptr);
+    if (lane == L) mine = t;
+  }
+  return mine;
+}
+
 // Thread-private top-k state of one lane (one query per lane).
+//
+// Threshold sharing: every state of query q (other lanes, warps and CTAs) publishes
+// its k-th best key to gthr[q] with atomicMax, and reads it back now and then.  Any
+// state's k-th best is a lower bound of the final k-th best of the whole shard, so
+// discarding keys <= max(published) is exact and cuts inserts to ~the single-state
+// rate no matter how the rows are split across threads.
 template <int P>
 struct LaneTopk {
   static constexpr int CAP = 32 * P;
-  uint64_t thr;   // every kept key is > thr once thr != 0 (k-th best after a compaction)
+  uint64_t thr;   // discard keys <= thr
+  float tlim;     // conservative score pre-filter: key > thr implies dot >= tlim * den
   int cnt;        // keys in buf
   uint64_t* buf;  // CAP keys, private to this lane
+  unsigned long long* g;  // shared threshold of this lane's query (nullptr: none)
 
-  __device__ __forceinline__ void init(uint64_t* b) { thr = 0; cnt = 0; buf = b; }
+  __device__ __forceinline__ void init(uint64_t* b, unsigned long long* gt) {
+    thr = 0; tlim = -__int_as_float(0x7f800000); cnt = 0; buf = b; g = gt;
+  }
+
+  __device__ __forceinline__ void raise(uint64_t t) {
+    if (t > thr) {
+      thr = t;
+      // a score s = RN(dot / den) (den > 0) can beat thr only if dot >= tlim * den:
+      // tlim sits 2^-18 (relative) below thr's score, far more than the few-ulp
+      // rounding of the division and of tlim * den
+      const float ts = key_score(t);
+      tlim = ts - fabsf(ts) * 3.814697265625e-06f - 1e-30f;
+    }
+  }
+
+  __device__ __forceinline__ uint64_t peek_shared() const {
+    return g ? *reinterpret_cast<volatile unsigned long long*>(g) : 0ull;
+  }
+
+  __device__ __forceinline__ bool may_pass(float dot, float den) const { return dot >= tlim * den; }
 
   // Whole warp calls with one key per lane (0 = nothing to offer).
   __device__ __forceinline__ void push(uint64_t key, int k) {
-    const int lane = threadIdx.x & 31;
-    unsigned full = __ballot_sync(kFull, key > thr && cnt == CAP);
-    while (full) {
-      const int L = __ffs(full) - 1;
-      full &= full - 1;
-      uint64_t* b = (uint64_t*)__shfl_sync(kFull, (unsigned long long)buf, L);
-      const uint64_t t = warp_compact<P>(b, CAP, k, nullptr);
-      if (lane == L) { thr = t; cnt = k; }
+    const unsigned full = __ballot_sync(kFull, key > thr && cnt == CAP);
+    if (full) {
+      const uint64_t t = lane_compact_slow<P>(full, buf, k);
+      if ((full >> (threadIdx.x & 31)) & 1u) {
+        cnt = k;
+        if (g) atomicMax(g, (unsigned long long)t);
+        raise(t);
+      }
     }
     if (key > thr) buf[cnt++] = key;
   }
+
+  // Out-of-line push for hot loops (keeps the unrolled common path small): the
+  // state travels by value in registers.
+  struct State { uint64_t thr; float tlim; int cnt; };
+  __device__ __forceinline__ State save() const { return State{thr, tlim, cnt}; }
+  __device__ __forceinline__ void load(const State& s) { thr = s.thr; tlim = s.tlim; cnt = s.cnt; }
+  static __device__ __noinline__ State push_call(State st, uint64_t key, int k, uint64_t* b,
+                                                 unsigned long long* gt) {
+    LaneTopk t;
+    t.thr = st.thr; t.tlim = st.tlim; t.cnt = st.cnt; t.buf = b; t.g = gt;
+    t.push(key, k);
+    return t.save();
+  }
+  __device__ __forceinline__ void push_ool(uint64_t key, int k) { load(push_call(save(), key, k, buf, g)); }
 
   // Whole warp: write each lane's sorted best k to out_of(lane) (k keys, zero padded).
   __device__ __forceinline__ void flush(uint64_t* my_out, int k) {

@@ -9,10 +9,12 @@ namespace remoe {
 // ---------------------------------------------------------------- S0 / S1 norms
 // |x| = sqrt(sum_d x_d^2) (Eq. 11 denominator).  One warp per row; lane
 // partial sums over 16-byte chunks in ascending chunk order, fixed xor butterfly.
-__global__ void k_norms(const uint16_t* __restrict__ x, int64_t n, int dim, float* __restrict__ out) {
+__global__ void k_norms(const uint16_t* __restrict__ x, int64_t n, int dim, float* __restrict__ out,
+                        unsigned long long* __restrict__ zero_u64) {
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
+  if (zero_u64 && lane == 0) zero_u64[row] = 0ull;
   const uint16_t* xr = x + row * dim;
   float s = 0.f;
   for (int c = lane; c < (dim >> 3); c += 32) {
@@ -27,11 +29,12 @@ __global__ void k_norms(const uint16_t* __restrict__ x, int64_t n, int dim, floa
   if (lane == 0) out[row] = __fsqrt_rn(s);
 }
 
-cudaError_t launch_norms(const uint16_t* x, int64_t n, int dim, float* out, cudaStream_t st) {
+cudaError_t launch_norms(const uint16_t* x, int64_t n, int dim, float* out, cudaStream_t st,
+                         unsigned long long* zero_u64) {
   if (n <= 0) return cudaSuccess;
   const int wpb = 8;
   const int64_t grid = (n + wpb - 1) / wpb;
-  k_norms<<<(unsigned)grid, wpb * 32, 0, st>>>(x, n, dim, out);
+  k_norms<<<(unsigned)grid, wpb * 32, 0, st>>>(x, n, dim, out, zero_u64);
   return cudaGetLastError();
 }
 

@@ -136,14 +136,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan_simt(SimtScanParams p) {
   } else if (warp == kComputeWarps) {
     // ------------------------------------------------ epilogue: lane b owns query b
     LaneTopk<P> tk;
-    tk.init(p.cand_buf + ((size_t)cta * 32 + lane) * LaneTopk<P>::CAP);
+    tk.init(p.cand_buf + ((size_t)cta * 32 + lane) * LaneTopk<P>::CAP,
+            lane < p.nq ? p.gthr + lane : nullptr);
     for (int it = 0; it < n_iter; ++it) {
       const int sb = it & 1;
       const uint32_t sph = (uint32_t)(it >> 1) & 1u;
       const int64_t rbase = r0 + (int64_t)it * SR;
       const int rows = (int)((r1 - rbase) < SR ? (r1 - rbase) : SR);
       const float* Sb = S + sb * SR * BQ;
+      const uint64_t gt = tk.peek_shared();
       mbar_wait(&sfull[sb], sph);
+      tk.raise(gt);
       for (int r = 0; r < rows; ++r) {
         // host guarantees nq <= BQ
         const uint64_t key = lane < p.nq ? make_key(Sb[r * BQ + lane], p.gid_offset + rbase + r) : 0ull;

@@ -1,23 +1,426 @@
-// k_scan_tc.cu -- S2+S3 on the 5th-generation tensor cores (tcgen05).  (stub: filled next)
+// k_scan_tc.cu -- S2+S3 on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// score_ij = (q_i . x_j) / (|q_i||x_j| + sigma)  (Eq. 11, DESIGN R2),
+// exact per-CTA running top-k per query (BF top-alpha).
+//
+// Shape: D[q, j] = sum_k Q[q, k] X[j, k], a bf16 x bf16 -> fp32
+// contraction with M = queries (64 or 128 per pass), N = 128 store rows per tile,
+// K = D.  Both operands are K-major, exactly as they sit in HBM.
+//   * The query slab (A, M x D) is written into shared memory ONCE per CTA in the
+//     128-byte-swizzled K-major layout and stays resident: the only HBM stream is
+//     the store itself (the path is HBM-bound until B ~ 214).
+//   * Warp 0: TMA producer.  Store tiles [128 rows x 64 elems] (16 KB, SWIZZLE_128B)
+//     stream through an NST-deep mbarrier ring with cp.async.bulk.tensor.2d.
+//   * Warp 1: one thread issues tcgen05.mma.cta_group::1.kind::f16 (4 per K-block),
+//     accumulating into one of two TMEM accumulators (128 fp32 columns each), and
+//     tcgen05.commit's the smem slot / the finished accumulator to mbarriers.
+//   * Warps 2-5: epilogue, one thread per query.  tcgen05.ld.32x32b.x32 gives thread (quarter w, lane t)
+//     query m's scores for 32 consecutive store rows; Eq. 11 scaling, key packing and
+//     a register-threshold compare per score; rare inserts go to the thread's private
+//     candidate buffer (LaneTopk, common.cuh).
+// The dot for (q, row) accumulates K-blocks in ascending order inside the tensor core;
+// it does not depend on the query's batch position, on M, or on the sharding.
+#include <cuda.h>
+#include <stdlib.h>
+
+#include "common.cuh"
+#include "kernels.h"
 #include "tc_host.h"
 
 namespace remoe {
 
+namespace {
+constexpr int kTileN = 128;          // store rows per tile (UMMA N)
+constexpr int kBlockK = 64;          // bf16 elements per 128-byte swizzle row
+constexpr int kStageBytes = kTileN * kBlockK * 2;  // 16 KB
+constexpr int kThreads = 192;        // 6 warps: TMA, MMA, 4 epilogue
+constexpr int kAcc = 4;              // TMEM accumulator stages
+constexpr int kTmemCols = kAcc * kTileN;
+constexpr int kMaxSmem = 232448;     // 227 KB opt-in
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+  // K-major, SWIZZLE_128B: start>>4 | LBO(16B)>>4 << 16 | SBO(1024B)>>4 << 32 | version 1 | layout 2
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct TcArgs {
+  const float* xnorm;
+  int64_t n_rows;
+  int64_t gid_offset;
+  int dim;
+  const uint16_t* q;
+  const float* qnorm;
+  int nq;
+  int k;
+  float sigma;
+  int n_stages;
+  uint64_t* cand_buf;
+  unsigned long long* gthr;  // [nq] shared thresholds (zeroed before the launch)
+  uint64_t* out;
+  int smem_bufs;  // candidate buffers in shared memory (else cand_buf in global memory)
+};
+}  // namespace
+
+// M = queries per pass (UMMA M, 64 or 128).  For M = 64 the accumulator rows live in
+// lanes 0-15 of each 32-lane TMEM quarter (row m -> lane 32*(m/16) + m%16).
+template <int M, int P>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_scan_tc(const __grid_constant__ CUtensorMap tmap_x, TcArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int D = p.dim;
+  const int nkb = D / kBlockK;  // host guarantees D % 64 == 0
+  const int NST = p.n_stages;
+  uint8_t* sA = smem;                                   // [nkb][M rows][128 B] swizzled
+  uint8_t* sB = sA + (size_t)nkb * M * 128;             // [NST][128 rows][128 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)NST * kStageBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + NST;
+  uint64_t* tfull = bars + 2 * NST;
+  uint64_t* tempty = bars + 2 * NST + kAcc;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NST + 2 * kAcc);
+  float* sXn = reinterpret_cast<float*>(bars + 2 * NST + 2 * kAcc + 2);  // [4 warps][128] x-norms
+  uint64_t* sBuf = reinterpret_cast<uint64_t*>(sXn + 4 * kTileN);  // [128][CAP] if p.smem_bufs
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t n_tiles = (p.n_rows + kTileN - 1) / kTileN;
+
+  // ---- one-time setup: barriers, TMEM, the resident query slab
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < kAcc; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
+    fence_mbar_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_x) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  {
+    // Q[m][kb*64 + c*8 .. +8] -> sA + kb*M*128 + m*128 + ((c ^ (m & 7)) * 16)  (SWIZZLE_128B)
+    const int chunks = M * (D / 8);
+    for (int i = threadIdx.x; i < chunks; i += blockDim.x) {
+      const int m = i / (D / 8);
+      const int cc = i - m * (D / 8);
+      const int kb = cc >> 3, c = cc & 7;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (m < p.nq) v = *reinterpret_cast<const uint4*>(p.q + (size_t)m * D + cc * 8);
+      *reinterpret_cast<uint4*>(sA + (size_t)kb * M * 128 + m * 128 + ((c ^ (m & 7)) << 4)) = v;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % NST;
+          const uint32_t ph = (uint32_t)(it / NST) & 1u;
+          mbar_wait(&empty[s], ph ^ 1u);
+          mbar_arrive_expect_tx(&full[s], kStageBytes);
+          tma_load_2d(sB + (size_t)s * kStageBytes, &tmap_x, kb * kBlockK, (int)(t * kTileN), &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (one thread)
+    if (lane == 0) {
+      // kind::f16: D fp32 (bit 4), A bf16 (bits 7-9 = 1), B bf16 (bits 10-12 = 1),
+      // both K-major, N >> 3 at bit 17, M >> 4 at bit 24
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTileN >> 3) << 17) |
+                             ((uint32_t)(M >> 4) << 24);
+      const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+      int it = 0, i = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+        const int acc = i % kAcc;
+        const uint32_t aph = (uint32_t)(i / kAcc) & 1u;
+        mbar_wait(&tempty[acc], aph ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kTileN);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % NST;
+          const uint32_t ph = (uint32_t)(it / NST) & 1u;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t abase = a0 + (uint32_t)(kb * M * 128);
+          const uint32_t bbase = b0 + (uint32_t)(s * kStageBytes);
+#pragma unroll
+          for (int kk = 0; kk < kBlockK / 16; ++kk)
+            umma_bf16(d_tmem, umma_desc(abase + kk * 32), umma_desc(bbase + kk * 32), idesc,
+                      (kb | kk) != 0);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue warps 2..5
+    // One warp per TMEM lane quarter (quarter = warp % 4 is the hardware rule), one
+    // thread per query: thread (quarter, t) owns query m and sees all 128 columns of
+    // every tile, so each query has exactly one top-k state per CTA.  For M = 64 the
+    // queries sit in lanes 0-15 of a quarter and lanes 16-31 idle.
+    //
+    // Per 32-column chunk the common path is branch-free: x-norms come from a per-warp
+    // shared-memory copy (ld.shared.v4 broadcasts), and a conservative fp32 test
+    // dot >= tlim * (|q||x| + sigma) builds a 32-bit candidate mask; only columns in
+    // the mask (rare once the threshold has settled) get the IEEE division, the key
+    // and the push.
+    const int quarter = warp & 3;
+    const int m = (M == 128) ? quarter * 32 + lane : quarter * 16 + lane;
+    const bool active = (M == 128 || lane < 16) && m < p.nq;
+    const float qn = active ? p.qnorm[m] : 0.f;
+    const int slot = quarter * 32 + lane;
+    float* xs = sXn + (warp - 2) * kTileN;  // this warp's copy of the tile's |x_j|
+    uint64_t* buf = p.smem_bufs ? sBuf + (size_t)slot * LaneTopk<P>::CAP
+                                : p.cand_buf + ((size_t)blockIdx.x * 128 + slot) * LaneTopk<P>::CAP;
+    LaneTopk<P> tk;
+    tk.init(buf, active ? p.gthr + m : nullptr);
+    if (!active) tk.tlim = __int_as_float(0x7f800000);  // +inf: never a candidate
+    int i = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+      const int acc = i % kAcc;
+      const uint32_t aph = (uint32_t)(i / kAcc) & 1u;
+      const int64_t row0 = t * kTileN;
+      const int nvalid = (int)((p.n_rows - row0) < kTileN ? (p.n_rows - row0) : kTileN);
+      // the tile's |x_j| (lane l loads rows 4l..4l+3), issued before the accumulator wait
+      float4 xv = make_float4(1.f, 1.f, 1.f, 1.f);
+      if (4 * lane + 3 < nvalid) {
+        xv = __ldg(reinterpret_cast<const float4*>(p.xnorm + row0) + lane);
+      } else {
+        if (4 * lane + 0 < nvalid) xv.x = __ldg(p.xnorm + row0 + 4 * lane + 0);
+        if (4 * lane + 1 < nvalid) xv.y = __ldg(p.xnorm + row0 + 4 * lane + 1);
+        if (4 * lane + 2 < nvalid) xv.z = __ldg(p.xnorm + row0 + 4 * lane + 2);
+      }
+      const uint64_t gt = tk.peek_shared();
+      __syncwarp();
+      reinterpret_cast<float4*>(xs)[lane] = xv;
+      __syncwarp();
+      mbar_wait(&tfull[acc], aph);
+      if (active) tk.raise(gt);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kTileN);
+#pragma unroll 1
+      for (int c = 0; c < kTileN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tbase + c * 32, v);
+        tmem_wait_ld();
+        if (c == kTileN / 32 - 1) {  // every load of this accumulator has completed
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        const float* xc = xs + c * 32;
+        unsigned mask = 0;
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 x4 = lds128f(xc + 4 * j4);
+          const float xx[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = 4 * j4 + u;
+            const float den = __fmaf_rn(qn, xx[u], p.sigma);
+            mask |= (tk.may_pass(__uint_as_float(v[j]), den) ? 1u : 0u) << j;
+          }
+        }
+        const int left = nvalid - c * 32;
+        if (left < 32) mask &= left > 0 ? ((1u << left) - 1u) : 0u;
+        if (__any_sync(kFull, mask != 0)) {
+          float vl[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) vl[j] = __uint_as_float(v[j]);
+          const int64_t gbase = p.gid_offset + row0 + c * 32;
+          while (__any_sync(kFull, mask != 0)) {
+            uint64_t key = 0;
+            if (mask) {
+              const int j = __ffs(mask) - 1;
+              mask &= mask - 1;
+              const float den = __fmaf_rn(qn, xc[j], p.sigma);
+              key = make_key(__fdiv_rn(vl[j], den), gbase + j);
+            }
+            tk.push(key, p.k);
+          }
+        }
+      }
+    }
+    uint64_t* out = active ? p.out + ((size_t)m * gridDim.x + blockIdx.x) * (size_t)p.k : nullptr;
+    tk.flush(out, p.k);
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols));
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+static size_t tc_smem(int M, int D, int nst, int buf_bytes) {
+  return 1024 + (size_t)(D / kBlockK) * M * 128 + (size_t)nst * kStageBytes +
+         (2 * (size_t)nst + 2 * kAcc + 2) * 8 + 4 * kTileN * 4 + (size_t)buf_bytes;
+}
+
+static int tc_stages(int M, int D, int buf_bytes) {
+  const long avail = (long)kMaxSmem - (long)tc_smem(M, D, 0, buf_bytes);
+  const long n = avail / (kStageBytes + 16);
+  return (int)(n > 8 ? 8 : n);
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
 remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int dim, int num_sms,
                               int max_k) {
-  (void)x; (void)n_rows; (void)dim; (void)num_sms; (void)max_k;
+  (void)max_k;
   t->ok = false;
-  t->why = "tensor-core scan not built yet";
+  t->x = x;
+  t->n_rows = n_rows;
+  t->dim = dim;
   t->grid = 0;
-  t->threads_per_cta_queries = 0;
+  t->threads_per_cta_queries = kTcEpilogueThreads;
+  if (dim % kBlockK != 0) { t->why = "D % 64 != 0"; return REMOE_OK; }
+  if (tc_stages(64, dim, 0) < 3) { t->why = "query slab does not fit shared memory (D > 1536)"; return REMOE_OK; }
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      fn == nullptr || q != cudaDriverEntryPointSuccess) {
+    cudaGetLastError();
+    t->why = "cuTensorMapEncodeTiled unavailable";
+    return REMOE_OK;
+  }
+  const cuuint64_t gdim[2] = {(cuuint64_t)dim, (cuuint64_t)n_rows};
+  const cuuint64_t gstride[1] = {(cuuint64_t)dim * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)kBlockK, (cuuint32_t)kTileN};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = ((EncodeTiledFn)fn)(reinterpret_cast<CUtensorMap*>(t->tmap_x), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                   const_cast<uint16_t*>(x), gdim, gstride, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { t->why = "cuTensorMapEncodeTiled failed"; return REMOE_OK; }
+  const int64_t n_tiles = (n_rows + kTileN - 1) / kTileN;
+  t->grid = (int)(n_tiles < num_sms ? n_tiles : num_sms);
+  t->ok = true;
+  t->why = "";
   return REMOE_OK;
 }
 
 void tc_plan_destroy(TcPlan* t) { t->ok = false; }
 
-remoe_status_t tc_scan(TcPlan*, const uint16_t*, const float*, int, int, float, const float*, int64_t,
-                       int64_t, uint64_t*, uint64_t*, cudaStream_t, int*) {
-  return REMOE_ERR_UNSUPPORTED;
+template <int M, int P>
+static cudaError_t launch_tc_t(const TcPlan* t, const TcArgs& a, cudaStream_t st) {
+  const size_t smem = tc_smem(M, a.dim, a.n_stages, a.smem_bufs ? 128 * 32 * P * 8 : 0);
+  auto kern = k_scan_tc<M, P>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<t->grid, kThreads, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(t->tmap_x), a);
+  return cudaGetLastError();
+}
+
+template <int M>
+static cudaError_t launch_tc_m(const TcPlan* t, const TcArgs& a, cudaStream_t st) {
+  switch (topk_P(a.k)) {
+    case 2: return launch_tc_t<M, 2>(t, a, st);
+    case 4: return launch_tc_t<M, 4>(t, a, st);
+    case 8: return launch_tc_t<M, 8>(t, a, st);
+    case 16: return launch_tc_t<M, 16>(t, a, st);
+    case 32: return launch_tc_t<M, 32>(t, a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc, int k, float sigma,
+                       const float* xnorm, int64_t n_rows, int64_t gid_offset, uint64_t* cand_buf,
+                       unsigned long long* gthr, uint64_t* lists, cudaStream_t st, int* launches,
+                       int* lists_per_query) {
+  if (!t->ok) return REMOE_ERR_UNSUPPORTED;
+  // M = 128 when the 128-query slab still leaves >= 4 stages, else 64.  Candidate
+  // buffers go to shared memory when that still leaves >= 4 stages.
+  const int M = tc_stages(128, t->dim, 0) >= 4 ? 128 : 64;
+  const int buf_bytes = 128 * 32 * topk_P(k) * 8;
+  const bool smem_bufs = tc_stages(M, t->dim, buf_bytes) >= 4 && !getenv("REMOE_TC_GLOBAL_BUFS");
+  int nst = tc_stages(M, t->dim, smem_bufs ? buf_bytes : 0);
+  if (const char* e = getenv("REMOE_TC_STAGES")) { const int v = atoi(e); if (v >= 2 && v < nst) nst = v; }
+  *lists_per_query = t->grid;
+  for (int s0 = 0; s0 < bc; s0 += M) {
+    TcArgs a{};
+    a.xnorm = xnorm;
+    a.n_rows = n_rows;
+    a.gid_offset = gid_offset;
+    a.dim = t->dim;
+    a.q = q + (size_t)s0 * t->dim;
+    a.qnorm = qnorm + s0;
+    a.nq = bc - s0 < M ? bc - s0 : M;
+    a.k = k;
+    a.sigma = sigma;
+    a.n_stages = nst;
+    a.cand_buf = cand_buf;
+    a.gthr = gthr + s0;
+    a.out = lists + (size_t)s0 * t->grid * k;
+    a.smem_bufs = smem_bufs ? 1 : 0;
+    cudaError_t e = (M == 128) ? launch_tc_m<128>(t, a, st) : launch_tc_m<64>(t, a, st);
+    if (e != cudaSuccess) return REMOE_ERR_CUDA;
+    ++*launches;
+  }
+  return REMOE_OK;
 }
 
 }  // namespace remoe

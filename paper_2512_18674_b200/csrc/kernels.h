@@ -22,29 +22,18 @@ struct SimtScanParams {
   int stage_rows;         // rows per TMA stage
   int n_stages_ring;      // ring depth
   uint64_t* cand_buf;     // [grid][32][CAP] private lane buffers
+  unsigned long long* gthr;  // [nq] shared per-query thresholds (zeroed by launch_norms)
   uint64_t* out;          // [nq][grid][k]
 };
 size_t simt_smem_bytes(int BQ, int dim, int stage_rows, int n_stages_ring);
 cudaError_t launch_scan_simt(const SimtScanParams& p, int BQ, int grid, cudaStream_t st);
 
 // S2+S3, tensor-core (tcgen05) variant; see k_scan_tc.cu.
-struct TcScanParams {
-  const void* tmap_x;     // CUtensorMap* (host-encoded, passed by value via __grid_constant__)
-  const float* xnorm;
-  int64_t n_rows;
-  int64_t gid_offset;
-  int dim;
-  const uint16_t* q;      // [nq][dim]
-  const float* qnorm;
-  int nq;                 // queries in this pass (<= 128 per M tile)
-  int k;
-  float sigma;
-  uint64_t* cand_buf;
-  uint64_t* out;          // [nq][grid][k]
-};
 
-// S1 / S0: L2 norms of bf16 rows (fp32, fixed order).
-cudaError_t launch_norms(const uint16_t* x, int64_t n, int dim, float* out, cudaStream_t st);
+// S1 / S0: L2 norms of bf16 rows (fp32, fixed order).  If zero_u64 is non-null,
+// zero_u64[row] = 0 as well (resets the per-query shared thresholds for free).
+cudaError_t launch_norms(const uint16_t* x, int64_t n, int dim, float* out, cudaStream_t st,
+                         unsigned long long* zero_u64 = nullptr);
 
 // S4 / S5: per query, merge n_lists sorted key lists of length k into the best k.
 // key(b, l, i) = in[b * qstride + l * lstride + i].

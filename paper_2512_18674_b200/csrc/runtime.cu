@@ -93,6 +93,7 @@ struct remoe_sps {
   float* act = nullptr;
   // workspaces
   float* qnorm = nullptr;
+  unsigned long long* gthr = nullptr;
   uint64_t* cand_buf = nullptr;
   uint64_t* lists = nullptr;
   uint64_t* local_top = nullptr;
@@ -287,12 +288,14 @@ static remoe_status_t build_impl(remoe_sps* h, const uint16_t* emb, const float*
   const int capmax = 32 * remoe::topk_P(c.max_k);
   ST_TRY(remoe::tc_plan_create(&h->tc, h->x, c.n_local, c.dim, h->num_sms, c.max_k));
   h->grid_tc = h->tc.grid;
-  const int grid_max = std::max(h->grid_simt, h->grid_tc);
-  const int lanes_max = std::max(32, h->tc.threads_per_cta_queries);
+  const int lists_max = std::max(h->grid_simt, h->grid_tc * remoe::kTcMaxStatesPerCta);
+  const size_t cand_lanes = std::max((size_t)h->grid_simt * 32,
+                                     (size_t)h->grid_tc * h->tc.threads_per_cta_queries);
   const int mb = c.max_batch;
   ST_TRY(h->alloc((void**)&h->qnorm, (size_t)mb * 4));
-  ST_TRY(h->alloc((void**)&h->cand_buf, (size_t)grid_max * lanes_max * capmax * 8));
-  ST_TRY(h->alloc((void**)&h->lists, (size_t)mb * grid_max * c.max_k * 8));
+  ST_TRY(h->alloc((void**)&h->gthr, (size_t)mb * 8));
+  ST_TRY(h->alloc((void**)&h->cand_buf, cand_lanes * capmax * 8));
+  ST_TRY(h->alloc((void**)&h->lists, (size_t)mb * lists_max * c.max_k * 8));
   ST_TRY(h->alloc((void**)&h->local_top, (size_t)mb * c.max_k * 8));
   ST_TRY(h->alloc((void**)&h->global_top, (size_t)mb * c.max_k * 8));
   if (c.world > 1) {
@@ -340,13 +343,13 @@ remoe_status_t remoe_sps_build(const remoe_sps_config_t* cfg, const uint16_t* em
 static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k, int64_t* ids,
                                   float* scores, float* pred, cudaStream_t st, int* launches) {
   const remoe_sps_config_t& c = h->cfg;
-  CUDA_TRY(remoe::launch_norms(q, bc, c.dim, h->qnorm, st));
+  CUDA_TRY(remoe::launch_norms(q, bc, c.dim, h->qnorm, st, h->gthr));
   ++*launches;
   // ---- S2+S3
   int which = h->force_kernel;
   if (which == 0) which = (bc <= remoe::kSimtMaxB || !h->tc.ok) ? 1 : 2;
   if (which == 2 && !h->tc.ok) return fail(REMOE_ERR_UNSUPPORTED, "tensor-core scan unavailable: %s", h->tc.why);
-  int grid = 0;
+  int grid = 0;  // sorted key lists per query produced by the scan
   CUDA_TRY(h->prof_mark(st, true));
   if (which == 1) {
     grid = h->grid_simt;
@@ -359,16 +362,17 @@ static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k
       p.dim = c.dim; p.q = q + (size_t)s0 * c.dim; p.qnorm = h->qnorm + s0;
       p.nq = std::min(BQ, bc - s0); p.k = k; p.sigma = c.sigma;
       p.stage_rows = h->stage_rows; p.n_stages_ring = NST;
-      p.cand_buf = h->cand_buf; p.out = h->lists + (size_t)s0 * grid * k;
+      p.cand_buf = h->cand_buf; p.gthr = h->gthr + s0; p.out = h->lists + (size_t)s0 * grid * k;
       CUDA_TRY(remoe::launch_scan_simt(p, BQ, grid, st));
       ++*launches;
       ++h->prof_launches;
     }
   } else {
-    grid = h->grid_tc;
     int nl = 0;
-    ST_TRY(remoe::tc_scan(&h->tc, q, h->qnorm, bc, k, c.sigma, h->xnorm, c.n_local, c.global_offset,
-                          h->cand_buf, h->lists, st, &nl));
+    const remoe_status_t ts = remoe::tc_scan(&h->tc, q, h->qnorm, bc, k, c.sigma, h->xnorm, c.n_local,
+                                             c.global_offset, h->cand_buf, h->gthr, h->lists, st, &nl, &grid);
+    if (ts != REMOE_OK)
+      return fail(ts, "tensor-core scan launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     *launches += nl;
     h->prof_launches += nl;
   }

@@ -8,13 +8,13 @@
 namespace remoe {
 
 // Batches up to this size use the streaming CUDA-core scan when both are legal.
-constexpr int kSimtMaxB = 4;
+constexpr int kSimtMaxB = 0;  // the tensor-core scan is faster at every measured B (profiles/)
 
 struct TcPlan {
   bool ok = false;            // tensor-core scan usable for this store
   const char* why = "not initialised";
   int grid = 0;               // persistent CTAs
-  int threads_per_cta_queries = 0;  // per-CTA private top-k lanes (queries per pass)
+  int threads_per_cta_queries = 0;  // per-CTA private top-k lanes
   alignas(64) unsigned char tmap_x[128];  // CUtensorMap of the store (bf16 [n][D], K-major)
   const uint16_t* x = nullptr;
   int64_t n_rows = 0;
@@ -24,10 +24,15 @@ struct TcPlan {
 remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int dim, int num_sms,
                               int max_k);
 void tc_plan_destroy(TcPlan* t);
-// Scores bc queries (any bc >= 1; internally 128 queries per pass) and writes per-CTA
-// sorted top-k key lists lists[(b * grid + cta) * k + i].
+// Scores bc queries (any bc >= 1; 64 or 128 queries per pass) and writes sorted
+// top-k key lists: *lists_per_query lists of k keys per query,
+// lists[(b * lists_per_query + l) * k + i].
 remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc, int k, float sigma,
                        const float* xnorm, int64_t n_rows, int64_t gid_offset, uint64_t* cand_buf,
-                       uint64_t* lists, cudaStream_t st, int* launches);
+                       unsigned long long* gthr, uint64_t* lists, cudaStream_t st, int* launches,
+                       int* lists_per_query);
+// Largest lists_per_query tc_scan can produce (workspace sizing).
+constexpr int kTcMaxStatesPerCta = 1;
+constexpr int kTcEpilogueThreads = 128;
 
 }  // namespace remoe
