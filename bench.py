@@ -203,15 +203,11 @@ def run_ours(args):
     # ---- inputs: this rank's shard, generated on the host, copied into HBM at build
     x = gen.store_emb(cfg.store_seed, cfg.n, cfg.dim, off, n_loc)
     a = gen.store_act(cfg.store_seed, cfg.n, cfg.layers, cfg.experts, cfg.moe_topk, off, n_loc)
-    uid = None
     if world > 1:
-        t = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            t.copy_(torch.frombuffer(bytearray(remoe.remoe_nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(t, 0)
-        uid = bytes(t.cpu().numpy())
-    sps = remoe.Sps(x, a, max_batch=max(B, 1), max_k=max(k, 1), device=local, rank=rank,
-                    world=world, global_offset=off, nccl_unique_id=uid)
+        from paper_2512_18674_b200.dist import build_sharded
+        sps = build_sharded(x, a, cfg.n, device=local, max_batch=max(B, 1), max_k=max(k, 1))
+    else:
+        sps = remoe.Sps(x, a, max_batch=max(B, 1), max_k=max(k, 1), device=local)
     if args.kernel != "auto":
         sps.set_kernel(remoe.KERNEL_STREAM if args.kernel == "stream" else remoe.KERNEL_TC)
 
