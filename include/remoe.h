@@ -170,9 +170,10 @@ REMOE_API remoe_status_t remoe_sps_set_kernel(remoe_sps_t h, int32_t which);
 
 /*
  * Live kernel timing for benchmarks.  enable = 1 starts recording CUDA events on
- * the query stream around every scan-kernel launch (S2+S3); each call returns
- * (after synchronizing those events) the accumulated scan time in ms and the
- * number of scan launches since the previous call, then resets them.
+ * the query stream around the S2+S3 phase of every query chunk (the scan kernel
+ * launches of that chunk, including the threshold-seeding scan when it runs); each
+ * call returns (after synchronizing those events) the accumulated phase time in ms
+ * and the number of phases since the previous call, then resets them.
  * enable = 0 stops recording.  scan_ms / launches may be NULL.
  */
 REMOE_API remoe_status_t remoe_sps_profile(remoe_sps_t h, int32_t enable, double* scan_ms,

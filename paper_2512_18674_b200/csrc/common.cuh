@@ -120,14 +120,15 @@ __device__ __forceinline__ uint64_t warp_compact(uint64_t* buf, int cnt, int k, 
 // Slow path of LaneTopk::push (rare, kept out of line): compact the full buffer of
 // every lane named in `full` (warp-uniform); returns this lane's new threshold.
 template <int P>
-__device__ __noinline__ uint64_t lane_compact_slow(unsigned full, uint64_t* mybuf, int k) {
+__device__ __noinline__ uint64_t lane_compact_slow(unsigned full, uint64_t* mybuf, int mycnt, int k) {
   const int lane = threadIdx.x & 31;
   uint64_t mine = 0;
   while (full) {
     const int L = __ffs(full) - 1;
     full &= full - 1;
     uint64_t* b = (uint64_t*)__shfl_sync(kFull, (unsigned long long)mybuf, L);
-    const uint64_t t = warp_compact<P>(b, 32 * P, k, nullptr);
+    const int c = __shfl_sync(kFull, mycnt, L);
+    const uint64_t t = warp_compact<P>(b, c, k, nullptr);
     if (lane == L) mine = t;
   }
   return mine;
@@ -170,17 +171,33 @@ struct LaneTopk {
 
   __device__ __forceinline__ bool may_pass(float dot, float den) const { return dot >= tlim * den; }
 
-  // Whole warp calls with one key per lane (0 = nothing to offer).
-  __device__ __forceinline__ void push(uint64_t key, int k) {
-    const unsigned full = __ballot_sync(kFull, key > thr && cnt == CAP);
-    if (full) {
-      const uint64_t t = lane_compact_slow<P>(full, buf, k);
-      if ((full >> (threadIdx.x & 31)) & 1u) {
-        cnt = k;
+  // Whole warp: compact the lanes in `full` (warp-uniform mask) down to their best k.
+  __device__ __forceinline__ void compact(unsigned full, int k) {
+    const uint64_t t = lane_compact_slow<P>(full, buf, cnt, k);
+    if ((full >> (threadIdx.x & 31)) & 1u) {
+      cnt = cnt < k ? cnt : k;
+      if (t) {
         if (g) atomicMax(g, (unsigned long long)t);
         raise(t);
       }
     }
+  }
+
+  // Whole warp: make room for `need` more keys in every lane's buffer (need <= CAP - k).
+  __device__ __forceinline__ void ensure_room(int need, int k) {
+    const unsigned full = __ballot_sync(kFull, cnt + need > CAP);
+    if (full) compact(full, k);
+  }
+
+  // Append without a capacity check (after ensure_room).
+  __device__ __forceinline__ void append(uint64_t key) {
+    if (key > thr) buf[cnt++] = key;
+  }
+
+  // Whole warp calls with one key per lane (0 = nothing to offer).
+  __device__ __forceinline__ void push(uint64_t key, int k) {
+    const unsigned full = __ballot_sync(kFull, key > thr && cnt == CAP);
+    if (full) compact(full, k);
     if (key > thr) buf[cnt++] = key;
   }
 
@@ -206,6 +223,64 @@ struct LaneTopk {
       const int c = __shfl_sync(kFull, cnt, L);
       if (o != nullptr) warp_compact<P>(b, c, k, o);
     }
+  }
+};
+
+// Register-resident top-K of one lane (K = pow2ceil(k) <= 16): a descending list
+// updated by an unrolled insertion network (~4 instructions per slot, no memory, no
+// warp sync).  The threshold is the K-th best seen (<= the k-th best: a valid, slightly
+// conservative bound) or the shared one, if higher; inserts stay near the
+// K(1 + ln(R/K)) rate of an exact running top-K.
+template <int K>
+struct RegTopk {
+  uint64_t L[K];
+  uint64_t thr;        // discard keys <= thr
+  uint64_t published;  // last value sent to g
+  float tlim;
+  int k;
+  unsigned long long* g;
+
+  __device__ __forceinline__ void init(int kk, unsigned long long* gt) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) L[j] = 0;
+    thr = 0; published = 0; tlim = -__int_as_float(0x7f800000); k = kk; g = gt;
+  }
+  __device__ __forceinline__ void raise(uint64_t t) {
+    if (t > thr) {
+      thr = t;
+      const float ts = key_score(t);
+      tlim = ts - fabsf(ts) * 3.814697265625e-06f - 1e-30f;  // see LaneTopk::raise
+    }
+  }
+  __device__ __forceinline__ uint64_t peek_shared() const {
+    return g ? *reinterpret_cast<volatile unsigned long long*>(g) : 0ull;
+  }
+  __device__ __forceinline__ bool may_pass(float dot, float den) const { return dot >= tlim * den; }
+
+  // Per lane (no warp sync); key 0 or key <= thr is a no-op.
+  __device__ __forceinline__ void insert(uint64_t x) {
+    if (x <= thr) return;
+#pragma unroll
+    for (int j = K - 1; j > 0; --j) {
+      const bool above_prev = x > L[j - 1];
+      L[j] = above_prev ? L[j - 1] : (x > L[j] ? x : L[j]);
+    }
+    L[0] = x > L[0] ? x : L[0];
+    raise(L[K - 1]);
+  }
+  // Share this lane's k-th best with the other states of its query (exact lower bound).
+  __device__ __forceinline__ void publish() {
+    if (g && thr > published) {
+      atomicMax(g, (unsigned long long)thr);
+      published = thr;
+    }
+  }
+  // Per lane: the sorted best k (zero padded) to out.
+  __device__ __forceinline__ void flush(uint64_t* out) const {
+    if (!out) return;
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (j < k) out[j] = L[j];
   }
 };
 

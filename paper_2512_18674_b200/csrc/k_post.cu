@@ -10,11 +10,12 @@ namespace remoe {
 // |x| = sqrt(sum_d x_d^2) (Eq. 11 denominator).  One warp per row; lane
 // partial sums over 16-byte chunks in ascending chunk order, fixed xor butterfly.
 __global__ void k_norms(const uint16_t* __restrict__ x, int64_t n, int dim, float* __restrict__ out,
-                        unsigned long long* __restrict__ zero_u64) {
+                        unsigned long long* __restrict__ zero_u64, int64_t zero_stride) {
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
   if (zero_u64 && lane == 0) zero_u64[row] = 0ull;
+  if (zero_u64 && zero_stride && lane == 1) zero_u64[row + zero_stride] = 0ull;
   const uint16_t* xr = x + row * dim;
   float s = 0.f;
   for (int c = lane; c < (dim >> 3); c += 32) {
@@ -30,11 +31,11 @@ __global__ void k_norms(const uint16_t* __restrict__ x, int64_t n, int dim, floa
 }
 
 cudaError_t launch_norms(const uint16_t* x, int64_t n, int dim, float* out, cudaStream_t st,
-                         unsigned long long* zero_u64) {
+                         unsigned long long* zero_u64, int64_t zero_stride) {
   if (n <= 0) return cudaSuccess;
   const int wpb = 8;
   const int64_t grid = (n + wpb - 1) / wpb;
-  k_norms<<<(unsigned)grid, wpb * 32, 0, st>>>(x, n, dim, out, zero_u64);
+  k_norms<<<(unsigned)grid, wpb * 32, 0, st>>>(x, n, dim, out, zero_u64, zero_stride);
   return cudaGetLastError();
 }
 
@@ -44,7 +45,8 @@ cudaError_t launch_norms(const uint16_t* x, int64_t n, int dim, float* out, cuda
 template <int P>
 __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, int n_lists,
                                                int64_t qstride, int64_t lstride, int k,
-                                               uint64_t* __restrict__ out) {
+                                               uint64_t* __restrict__ out,
+                                               unsigned long long* __restrict__ set_thr) {
   constexpr int CAP = 32 * P;
   extern __shared__ __align__(16) uint64_t msm[];
   uint64_t* buf = msm;               // [8][CAP]
@@ -74,28 +76,37 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
         tk.push(key, k);
       }
     tk.finish(out + (int64_t)b * k, k);
+    if (set_thr) {
+      // seeding: the k-th best key of a subset of rows, minus one (strict lower bound,
+      // the subset's own rows stay admissible in the full scan)
+      __syncwarp();
+      if (lane == 0) {
+        const uint64_t kth = out[(int64_t)b * k + k - 1];
+        set_thr[b] = kth ? kth - 1 : 0ull;
+      }
+    }
   }
 }
 
 template <int P>
 static cudaError_t merge_t(const uint64_t* in, int B, int n_lists, int64_t qstride, int64_t lstride,
-                           int k, uint64_t* out, cudaStream_t st) {
+                           int k, uint64_t* out, unsigned long long* set_thr, cudaStream_t st) {
   const size_t smem = (size_t)8 * (32 * P + k) * sizeof(uint64_t);
   cudaError_t e = cudaFuncSetAttribute(k_merge<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_merge<P><<<B, 256, smem, st>>>(in, n_lists, qstride, lstride, k, out);
+  k_merge<P><<<B, 256, smem, st>>>(in, n_lists, qstride, lstride, k, out, set_thr);
   return cudaGetLastError();
 }
 
 cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride, int64_t lstride,
-                         int k, uint64_t* out, cudaStream_t st) {
+                         int k, uint64_t* out, cudaStream_t st, unsigned long long* set_thr) {
   if (B <= 0) return cudaSuccess;
   switch (topk_P(k)) {  // WarpTopk needs CAP = 32*P >= k + 32: topk_P guarantees it
-    case 2: return merge_t<2>(in, B, n_lists, qstride, lstride, k, out, st);
-    case 4: return merge_t<4>(in, B, n_lists, qstride, lstride, k, out, st);
-    case 8: return merge_t<8>(in, B, n_lists, qstride, lstride, k, out, st);
-    case 16: return merge_t<16>(in, B, n_lists, qstride, lstride, k, out, st);
-    case 32: return merge_t<32>(in, B, n_lists, qstride, lstride, k, out, st);
+    case 2: return merge_t<2>(in, B, n_lists, qstride, lstride, k, out, set_thr, st);
+    case 4: return merge_t<4>(in, B, n_lists, qstride, lstride, k, out, set_thr, st);
+    case 8: return merge_t<8>(in, B, n_lists, qstride, lstride, k, out, set_thr, st);
+    case 16: return merge_t<16>(in, B, n_lists, qstride, lstride, k, out, set_thr, st);
+    case 32: return merge_t<32>(in, B, n_lists, qstride, lstride, k, out, set_thr, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -14,7 +14,7 @@
 //   * Warp 1: one thread issues tcgen05.mma.cta_group::1.kind::f16 (4 per K-block),
 //     accumulating into one of two TMEM accumulators (128 fp32 columns each), and
 //     tcgen05.commit's the smem slot / the finished accumulator to mbarriers.
-//   * Warps 2-5: epilogue, one thread per query.  tcgen05.ld.32x32b.x32 gives thread (quarter w, lane t)
+//   * Warps 2-9: epilogue, one thread per (query, tile parity).  tcgen05.ld.32x32b.x32 gives thread (quarter w, lane t)
 //     query m's scores for 32 consecutive store rows; Eq. 11 scaling, key packing and
 //     a register-threshold compare per score; rare inserts go to the thread's private
 //     candidate buffer (LaneTopk, common.cuh).
@@ -22,6 +22,8 @@
 // it does not depend on the query's batch position, on M, or on the sharding.
 #include <cuda.h>
 #include <stdlib.h>
+
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -33,7 +35,8 @@ namespace {
 constexpr int kTileN = 128;          // store rows per tile (UMMA N)
 constexpr int kBlockK = 64;          // bf16 elements per 128-byte swizzle row
 constexpr int kStageBytes = kTileN * kBlockK * 2;  // 16 KB
-constexpr int kThreads = 192;        // 6 warps: TMA, MMA, 4 epilogue
+constexpr int kThreads = 320;        // 10 warps: TMA, MMA, 8 epilogue
+constexpr int kEpiWarps = 8;
 constexpr int kAcc = 4;              // TMEM accumulator stages
 constexpr int kTmemCols = kAcc * kTileN;
 constexpr int kMaxSmem = 232448;     // 227 KB opt-in
@@ -106,12 +109,13 @@ struct TcArgs {
   unsigned long long* gthr;  // [nq] shared thresholds (zeroed before the launch)
   uint64_t* out;
   int smem_bufs;  // candidate buffers in shared memory (else cand_buf in global memory)
+  const int64_t* gid_map;  // global id of row r = gid_map[r] if non-null, else gid_offset + r
 };
 }  // namespace
 
 // M = queries per pass (UMMA M, 64 or 128).  For M = 64 the accumulator rows live in
 // lanes 0-15 of each 32-lane TMEM quarter (row m -> lane 32*(m/16) + m%16).
-template <int M, int P>
+template <int M, int P, int KR>
 __global__ void __launch_bounds__(kThreads, 1)
     k_scan_tc(const __grid_constant__ CUtensorMap tmap_x, TcArgs p) {
   extern __shared__ uint8_t smem_raw[];
@@ -127,8 +131,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = bars + 2 * NST;
   uint64_t* tempty = bars + 2 * NST + kAcc;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NST + 2 * kAcc);
-  float* sXn = reinterpret_cast<float*>(bars + 2 * NST + 2 * kAcc + 2);  // [4 warps][128] x-norms
-  uint64_t* sBuf = reinterpret_cast<uint64_t*>(sXn + 4 * kTileN);  // [128][CAP] if p.smem_bufs
+  float* sXn = reinterpret_cast<float*>(bars + 2 * NST + 2 * kAcc + 2);  // [8 warps][128] x-norms
+  uint64_t* sBuf = reinterpret_cast<uint64_t*>(sXn + kEpiWarps * kTileN);  // [256][CAP] if p.smem_bufs
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -147,23 +151,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                  "n"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  {
-    // Q[m][kb*64 + c*8 .. +8] -> sA + kb*M*128 + m*128 + ((c ^ (m & 7)) * 16)  (SWIZZLE_128B)
-    const int chunks = M * (D / 8);
-    for (int i = threadIdx.x; i < chunks; i += blockDim.x) {
-      const int m = i / (D / 8);
-      const int cc = i - m * (D / 8);
-      const int kb = cc >> 3, c = cc & 7;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (m < p.nq) v = *reinterpret_cast<const uint4*>(p.q + (size_t)m * D + cc * 8);
-      *reinterpret_cast<uint4*>(sA + (size_t)kb * M * 128 + m * 128 + ((c ^ (m & 7)) << 4)) = v;
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (warp != 0) {
+    // Warps 1-9 write the resident query slab while warp 0 already streams the store:
+    // Q[m][kb*64 + c*8 .. +8] -> sA + kb*M*128 + m*128 + ((c ^ (m & 7)) * 16)  (SWIZZLE_128B)
+    const int chunks = M * (D / 8);
+    const uint32_t a_s = smem_u32(sA);
+    for (int i = threadIdx.x - 32; i < chunks; i += blockDim.x - 32) {
+      const int m = i / (D / 8);
+      const int cc = i - m * (D / 8);
+      const int kb = cc >> 3, c = cc & 7;
+      const uint32_t dst = a_s + (uint32_t)(kb * M * 128 + m * 128 + ((c ^ (m & 7)) << 4));
+      const uint16_t* src = p.q + (size_t)(m < p.nq ? m : 0) * D + cc * 8;
+      const uint32_t bytes = m < p.nq ? 16u : 0u;  // src-size 0 -> zero fill
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes)
+                   : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(kThreads - 32) : "memory");  // warps 1-9 only
+  }
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
@@ -211,47 +221,67 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ------------------------------------------------ epilogue warps 2..5
-    // One warp per TMEM lane quarter (quarter = warp % 4 is the hardware rule), one
-    // thread per query: thread (quarter, t) owns query m and sees all 128 columns of
-    // every tile, so each query has exactly one top-k state per CTA.  For M = 64 the
-    // queries sit in lanes 0-15 of a quarter and lanes 16-31 idle.
+    // ------------------------------------------------ epilogue warps 2..9
+    // Two warps per TMEM lane quarter (quarter = warp % 4 is the hardware rule); the
+    // pair alternates tiles (parity = tile index % 2), so each warp has two tiles' time
+    // for one tile and the pair hides each other's latency.  One thread per (query,
+    // parity): thread (quarter, t) owns query m and sees all 128 columns of its tiles,
+    // i.e. two top-k states per query per CTA.  For M = 64 the queries sit in lanes
+    // 0-15 of a quarter and lanes 16-31 idle.
     //
     // Per 32-column chunk the common path is branch-free: x-norms come from a per-warp
     // shared-memory copy (ld.shared.v4 broadcasts), and a conservative fp32 test
     // dot >= tlim * (|q||x| + sigma) builds a 32-bit candidate mask; only columns in
     // the mask (rare once the threshold has settled) get the IEEE division, the key
     // and the push.
+    const int e = warp - 2;
     const int quarter = warp & 3;
+    const int parity = e >> 2;
     const int m = (M == 128) ? quarter * 32 + lane : quarter * 16 + lane;
     const bool active = (M == 128 || lane < 16) && m < p.nq;
     const float qn = active ? p.qnorm[m] : 0.f;
-    const int slot = quarter * 32 + lane;
-    float* xs = sXn + (warp - 2) * kTileN;  // this warp's copy of the tile's |x_j|
-    uint64_t* buf = p.smem_bufs ? sBuf + (size_t)slot * LaneTopk<P>::CAP
-                                : p.cand_buf + ((size_t)blockIdx.x * 128 + slot) * LaneTopk<P>::CAP;
-    LaneTopk<P> tk;
-    tk.init(buf, active ? p.gthr + m : nullptr);
+    const int slot = e * 32 + lane;
+    float* xs = sXn + e * kTileN;  // this warp's copy of the tile's |x_j|
+    constexpr int kCap = 32 * (P > 0 ? P : 2);
+    uint64_t* buf = p.smem_bufs ? sBuf + (size_t)slot * kCap
+                                : p.cand_buf + ((size_t)blockIdx.x * kTcEpilogueThreads + slot) * kCap;
+    // KR > 0: register top-KR (k <= KR <= 16); otherwise buffer + compaction (any k <= 256)
+    using Topk = typename std::conditional<(KR > 0), RegTopk<(KR > 0 ? KR : 1)>, LaneTopk<(P > 0 ? P : 2)>>::type;
+    Topk tk;
+    if constexpr (KR > 0) tk.init(p.k, active ? p.gthr + m : nullptr);
+    else tk.init(buf, active ? p.gthr + m : nullptr);
     if (!active) tk.tlim = __int_as_float(0x7f800000);  // +inf: never a candidate
-    int i = 0;
-    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+    // the tile's |x_j| (lane l loads rows 4l..4l+3) are loaded one tile ahead
+    auto load_xn = [&](int64_t t) {
+      float4 x = make_float4(1.f, 1.f, 1.f, 1.f);
+      if (t >= n_tiles) return x;
+      const int64_t r0 = t * kTileN;
+      const int nv = (int)((p.n_rows - r0) < kTileN ? (p.n_rows - r0) : kTileN);
+      if (4 * lane + 3 < nv) {
+        x = __ldg(reinterpret_cast<const float4*>(p.xnorm + r0) + lane);
+      } else {
+        if (4 * lane + 0 < nv) x.x = __ldg(p.xnorm + r0 + 4 * lane + 0);
+        if (4 * lane + 1 < nv) x.y = __ldg(p.xnorm + r0 + 4 * lane + 1);
+        if (4 * lane + 2 < nv) x.z = __ldg(p.xnorm + r0 + 4 * lane + 2);
+      }
+      return x;
+    };
+    const int64_t tstep = 2 * (int64_t)gridDim.x;
+    float4 xv_next = load_xn(blockIdx.x + parity * (int64_t)gridDim.x);
+    uint64_t gt_next = tk.peek_shared();  // shared threshold, also read one tile ahead
+    int i = parity;
+    for (int64_t t = blockIdx.x + parity * (int64_t)gridDim.x; t < n_tiles; t += tstep, i += 2) {
       const int acc = i % kAcc;
       const uint32_t aph = (uint32_t)(i / kAcc) & 1u;
       const int64_t row0 = t * kTileN;
       const int nvalid = (int)((p.n_rows - row0) < kTileN ? (p.n_rows - row0) : kTileN);
-      // the tile's |x_j| (lane l loads rows 4l..4l+3), issued before the accumulator wait
-      float4 xv = make_float4(1.f, 1.f, 1.f, 1.f);
-      if (4 * lane + 3 < nvalid) {
-        xv = __ldg(reinterpret_cast<const float4*>(p.xnorm + row0) + lane);
-      } else {
-        if (4 * lane + 0 < nvalid) xv.x = __ldg(p.xnorm + row0 + 4 * lane + 0);
-        if (4 * lane + 1 < nvalid) xv.y = __ldg(p.xnorm + row0 + 4 * lane + 1);
-        if (4 * lane + 2 < nvalid) xv.z = __ldg(p.xnorm + row0 + 4 * lane + 2);
-      }
-      const uint64_t gt = tk.peek_shared();
+      const float4 xv = xv_next;
+      const uint64_t gt = gt_next;
       __syncwarp();
       reinterpret_cast<float4*>(xs)[lane] = xv;
       __syncwarp();
+      xv_next = load_xn(t + tstep);
+      gt_next = tk.peek_shared();
       mbar_wait(&tfull[acc], aph);
       if (active) tk.raise(gt);
       tc_fence_after();
@@ -281,26 +311,68 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int left = nvalid - c * 32;
         if (left < 32) mask &= left > 0 ? ((1u << left) - 1u) : 0u;
-        if (__any_sync(kFull, mask != 0)) {
-          float vl[32];
+        if constexpr (KR > 0) {
+          if (__any_sync(kFull, mask != 0)) {
+            float vl[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) vl[j] = __uint_as_float(v[j]);
-          const int64_t gbase = p.gid_offset + row0 + c * 32;
-          while (__any_sync(kFull, mask != 0)) {
-            uint64_t key = 0;
-            if (mask) {
+            for (int j = 0; j < 32; ++j) vl[j] = __uint_as_float(v[j]);
+            const int64_t gbase = p.gid_offset + row0 + c * 32;
+            while (mask) {  // per lane: insertion network, no warp synchronisation
               const int j = __ffs(mask) - 1;
               mask &= mask - 1;
               const float den = __fmaf_rn(qn, xc[j], p.sigma);
-              key = make_key(__fdiv_rn(vl[j], den), gbase + j);
+              if (vl[j] >= tk.tlim * den) {
+                const int64_t gid = p.gid_map ? p.gid_map[row0 + c * 32 + j] : gbase + j;
+                tk.insert(make_key(__fdiv_rn(vl[j], den), gid));
+              }
             }
-            tk.push(key, p.k);
+          }
+        } else {
+          const int pc = __popc(mask);
+          if (__any_sync(kFull, pc >= 4)) {
+            // many candidates (the first tiles, before the thresholds settle): compute all
+            // keys of the chunk at once and append them (room for 32 guaranteed first)
+            tk.ensure_room(32, p.k);
+            const int64_t gbase = p.gid_offset + row0 + c * 32;
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4) {
+              const float4 x4 = lds128f(xc + 4 * j4);
+              const float xx[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int j = 4 * j4 + u;
+                if ((mask >> j) & 1u) {
+                  const float den = __fmaf_rn(qn, xx[u], p.sigma);
+                  const int64_t gid = p.gid_map ? p.gid_map[row0 + c * 32 + j] : gbase + j;
+                  tk.append(make_key(__fdiv_rn(__uint_as_float(v[j]), den), gid));
+                }
+              }
+            }
+          } else if (__any_sync(kFull, mask != 0)) {
+            float vl[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) vl[j] = __uint_as_float(v[j]);
+            const int64_t gbase = p.gid_offset + row0 + c * 32;
+            while (__any_sync(kFull, mask != 0)) {
+              uint64_t key = 0;
+              if (mask) {
+                const int j = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const float den = __fmaf_rn(qn, xc[j], p.sigma);
+                const int64_t gid = p.gid_map ? p.gid_map[row0 + c * 32 + j] : gbase + j;
+                key = make_key(__fdiv_rn(vl[j], den), gid);
+              }
+              tk.push(key, p.k);
+            }
           }
         }
       }
+      if constexpr (KR > 0) tk.publish();
     }
-    uint64_t* out = active ? p.out + ((size_t)m * gridDim.x + blockIdx.x) * (size_t)p.k : nullptr;
-    tk.flush(out, p.k);
+    uint64_t* out =
+        active ? p.out + (((size_t)m * gridDim.x + blockIdx.x) * 2 + parity) * (size_t)p.k : nullptr;
+    if constexpr (KR > 0) tk.flush(out);
+    else tk.flush(out, p.k);
   }
   __syncthreads();
   if (warp == 1) {
@@ -313,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 static size_t tc_smem(int M, int D, int nst, int buf_bytes) {
   return 1024 + (size_t)(D / kBlockK) * M * 128 + (size_t)nst * kStageBytes +
-         (2 * (size_t)nst + 2 * kAcc + 2) * 8 + 4 * kTileN * 4 + (size_t)buf_bytes;
+         (2 * (size_t)nst + 2 * kAcc + 2) * 8 + kEpiWarps * kTileN * 4 + (size_t)buf_bytes;
 }
 
 static int tc_stages(int M, int D, int buf_bytes) {
@@ -365,10 +437,11 @@ remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int 
 
 void tc_plan_destroy(TcPlan* t) { t->ok = false; }
 
-template <int M, int P>
+template <int M, int P, int KR = 0>
 static cudaError_t launch_tc_t(const TcPlan* t, const TcArgs& a, cudaStream_t st) {
-  const size_t smem = tc_smem(M, a.dim, a.n_stages, a.smem_bufs ? 128 * 32 * P * 8 : 0);
-  auto kern = k_scan_tc<M, P>;
+  const size_t smem = tc_smem(M, a.dim, a.n_stages, a.smem_bufs ? kTcEpilogueThreads * 32 * P * 8 : 0);
+  static_assert(P >= 0, "P");
+  auto kern = k_scan_tc<M, P, KR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<t->grid, kThreads, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(t->tmap_x), a);
@@ -377,6 +450,12 @@ static cudaError_t launch_tc_t(const TcPlan* t, const TcArgs& a, cudaStream_t st
 
 template <int M>
 static cudaError_t launch_tc_m(const TcPlan* t, const TcArgs& a, cudaStream_t st) {
+  // register top-k for k <= 16 (list length pow2ceil(k))
+  if (a.k <= 1) return launch_tc_t<M, 0, 1>(t, a, st);
+  if (a.k <= 2) return launch_tc_t<M, 0, 2>(t, a, st);
+  if (a.k <= 4) return launch_tc_t<M, 0, 4>(t, a, st);
+  if (a.k <= 8) return launch_tc_t<M, 0, 8>(t, a, st);
+  if (a.k <= 16) return launch_tc_t<M, 0, 16>(t, a, st);
   switch (topk_P(a.k)) {
     case 2: return launch_tc_t<M, 2>(t, a, st);
     case 4: return launch_tc_t<M, 4>(t, a, st);
@@ -388,18 +467,18 @@ static cudaError_t launch_tc_m(const TcPlan* t, const TcArgs& a, cudaStream_t st
 }
 
 remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc, int k, float sigma,
-                       const float* xnorm, int64_t n_rows, int64_t gid_offset, uint64_t* cand_buf,
-                       unsigned long long* gthr, uint64_t* lists, cudaStream_t st, int* launches,
-                       int* lists_per_query) {
+                       const float* xnorm, int64_t n_rows, int64_t gid_offset, const int64_t* gid_map,
+                       uint64_t* cand_buf, unsigned long long* gthr, uint64_t* lists, cudaStream_t st,
+                       int* launches, int* lists_per_query) {
   if (!t->ok) return REMOE_ERR_UNSUPPORTED;
   // M = 128 when the 128-query slab still leaves >= 4 stages, else 64.  Candidate
   // buffers go to shared memory when that still leaves >= 4 stages.
   const int M = tc_stages(128, t->dim, 0) >= 4 ? 128 : 64;
-  const int buf_bytes = 128 * 32 * topk_P(k) * 8;
-  const bool smem_bufs = tc_stages(M, t->dim, buf_bytes) >= 4 && !getenv("REMOE_TC_GLOBAL_BUFS");
+  const int buf_bytes = k <= 16 ? 0 : kTcEpilogueThreads * 32 * topk_P(k) * 8;
+  const bool smem_bufs = k > 16 && tc_stages(M, t->dim, buf_bytes) >= 4 && !getenv("REMOE_TC_GLOBAL_BUFS");
   int nst = tc_stages(M, t->dim, smem_bufs ? buf_bytes : 0);
   if (const char* e = getenv("REMOE_TC_STAGES")) { const int v = atoi(e); if (v >= 2 && v < nst) nst = v; }
-  *lists_per_query = t->grid;
+  *lists_per_query = t->grid * 2;
   for (int s0 = 0; s0 < bc; s0 += M) {
     TcArgs a{};
     a.xnorm = xnorm;
@@ -414,7 +493,8 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
     a.n_stages = nst;
     a.cand_buf = cand_buf;
     a.gthr = gthr + s0;
-    a.out = lists + (size_t)s0 * t->grid * k;
+    a.gid_map = gid_map;
+    a.out = lists + (size_t)s0 * t->grid * 2 * k;
     a.smem_bufs = smem_bufs ? 1 : 0;
     cudaError_t e = (M == 128) ? launch_tc_m<128>(t, a, st) : launch_tc_m<64>(t, a, st);
     if (e != cudaSuccess) return REMOE_ERR_CUDA;

@@ -33,12 +33,13 @@ cudaError_t launch_scan_simt(const SimtScanParams& p, int BQ, int grid, cudaStre
 // S1 / S0: L2 norms of bf16 rows (fp32, fixed order).  If zero_u64 is non-null,
 // zero_u64[row] = 0 as well (resets the per-query shared thresholds for free).
 cudaError_t launch_norms(const uint16_t* x, int64_t n, int dim, float* out, cudaStream_t st,
-                         unsigned long long* zero_u64 = nullptr);
+                         unsigned long long* zero_u64 = nullptr, int64_t zero_stride = 0);
 
 // S4 / S5: per query, merge n_lists sorted key lists of length k into the best k.
-// key(b, l, i) = in[b * qstride + l * lstride + i].
+// key(b, l, i) = in[b * qstride + l * lstride + i].  If set_thr is non-null, also
+// set_thr[b] = (k-th best key) - 1 (threshold seeding from a row sample).
 cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride, int64_t lstride,
-                         int k, uint64_t* out, cudaStream_t st);
+                         int k, uint64_t* out, cudaStream_t st, unsigned long long* set_thr = nullptr);
 
 // S6 + S7.  mode 0: rows come from the local table act[(gid - offset) * LE];
 // mode 1: rows come from rows[(b * k + r) * LE] (multi-GPU gathered winners).

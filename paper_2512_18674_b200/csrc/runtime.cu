@@ -107,6 +107,15 @@ struct remoe_sps {
   float* hpred = nullptr;
   // tensor-core path
   remoe::TcPlan tc{};
+  // threshold seeding: a strided sample of S rows, scanned first; its
+  // k-th best key - 1 is a strict lower bound that the full scan starts from
+  remoe::TcPlan tc_seed{};
+  int64_t seed_rows = 0;
+  uint16_t* xs = nullptr;
+  float* xns = nullptr;
+  int64_t* gids = nullptr;
+  uint64_t* seed_top = nullptr;
+  bool seed_enabled = false;  // REMOE_SEED=1: measured net-negative at small B so far
   ncclComm_t comm = nullptr;
   int force_kernel = 0;
   int last_kernel = 0;
@@ -162,6 +171,7 @@ struct remoe_sps {
     for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
     prof_ev.clear();
     remoe::tc_plan_destroy(&tc);
+    remoe::tc_plan_destroy(&tc_seed);
     if (comm) { ncclCommDestroy(comm); comm = nullptr; }
   }
 };
@@ -293,7 +303,27 @@ static remoe_status_t build_impl(remoe_sps* h, const uint16_t* emb, const float*
                                      (size_t)h->grid_tc * h->tc.threads_per_cta_queries);
   const int mb = c.max_batch;
   ST_TRY(h->alloc((void**)&h->qnorm, (size_t)mb * 4));
-  ST_TRY(h->alloc((void**)&h->gthr, (size_t)mb * 8));
+  ST_TRY(h->alloc((void**)&h->gthr, (size_t)2 * mb * 8));  // [0, mb): main scan, [mb, 2mb): seed scan
+  // ---- seeding sample: S rows j * stride, S a multiple of 128, only for large shards
+  if (h->tc.ok && c.n_local >= 32 * 2048) {
+    const int64_t S = 2048;
+    const int64_t stride = c.n_local / S;
+    h->seed_rows = S;
+    ST_TRY(h->alloc((void**)&h->xs, (size_t)S * c.dim * 2));
+    ST_TRY(h->alloc((void**)&h->xns, (size_t)S * 4));
+    ST_TRY(h->alloc((void**)&h->gids, (size_t)S * 8));
+    ST_TRY(h->alloc((void**)&h->seed_top, (size_t)mb * c.max_k * 8));
+    CUDA_TRY(cudaMemcpy2DAsync(h->xs, (size_t)c.dim * 2, h->x, (size_t)stride * c.dim * 2, (size_t)c.dim * 2, S,
+                               cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaMemcpy2DAsync(h->xns, 4, h->xnorm, (size_t)stride * 4, 4, S, cudaMemcpyDeviceToDevice, st));
+    std::vector<int64_t> g(S);
+    for (int64_t j = 0; j < S; ++j) g[j] = c.global_offset + j * stride;
+    CUDA_TRY(cudaMemcpyAsync(h->gids, g.data(), S * 8, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    ST_TRY(remoe::tc_plan_create(&h->tc_seed, h->xs, S, c.dim, h->num_sms, c.max_k));
+    if (!h->tc_seed.ok) h->seed_rows = 0;
+  }
+  if (const char* e = getenv("REMOE_SEED")) h->seed_enabled = atoi(e) != 0;
   ST_TRY(h->alloc((void**)&h->cand_buf, cand_lanes * capmax * 8));
   ST_TRY(h->alloc((void**)&h->lists, (size_t)mb * lists_max * c.max_k * 8));
   ST_TRY(h->alloc((void**)&h->local_top, (size_t)mb * c.max_k * 8));
@@ -343,7 +373,7 @@ remoe_status_t remoe_sps_build(const remoe_sps_config_t* cfg, const uint16_t* em
 static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k, int64_t* ids,
                                   float* scores, float* pred, cudaStream_t st, int* launches) {
   const remoe_sps_config_t& c = h->cfg;
-  CUDA_TRY(remoe::launch_norms(q, bc, c.dim, h->qnorm, st, h->gthr));
+  CUDA_TRY(remoe::launch_norms(q, bc, c.dim, h->qnorm, st, h->gthr, c.max_batch));
   ++*launches;
   // ---- S2+S3
   int which = h->force_kernel;
@@ -365,18 +395,28 @@ static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k
       p.cand_buf = h->cand_buf; p.gthr = h->gthr + s0; p.out = h->lists + (size_t)s0 * grid * k;
       CUDA_TRY(remoe::launch_scan_simt(p, BQ, grid, st));
       ++*launches;
-      ++h->prof_launches;
     }
   } else {
     int nl = 0;
+    if (h->seed_rows > 0 && h->seed_enabled && 8 * k <= h->seed_rows) {
+      int sl = 0;
+      const remoe_status_t ss = remoe::tc_scan(&h->tc_seed, q, h->qnorm, bc, k, c.sigma, h->xns, h->seed_rows,
+                                               0, h->gids, h->cand_buf, h->gthr + c.max_batch, h->lists, st,
+                                               &nl, &sl);
+      if (ss != REMOE_OK)
+        return fail(ss, "seed scan launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+      CUDA_TRY(remoe::launch_merge(h->lists, bc, sl, (int64_t)sl * k, k, k, h->seed_top, st, h->gthr));
+      ++nl;
+    }
     const remoe_status_t ts = remoe::tc_scan(&h->tc, q, h->qnorm, bc, k, c.sigma, h->xnorm, c.n_local,
-                                             c.global_offset, h->cand_buf, h->gthr, h->lists, st, &nl, &grid);
+                                             c.global_offset, nullptr, h->cand_buf, h->gthr, h->lists, st,
+                                             &nl, &grid);
     if (ts != REMOE_OK)
       return fail(ts, "tensor-core scan launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     *launches += nl;
-    h->prof_launches += nl;
   }
   CUDA_TRY(h->prof_mark(st, false));
+  ++h->prof_launches;  // one S2+S3 phase per query chunk
   h->last_kernel = which;
   // ---- S4
   uint64_t* top = h->local_top;

@@ -27,12 +27,13 @@ void tc_plan_destroy(TcPlan* t);
 // Scores bc queries (any bc >= 1; 64 or 128 queries per pass) and writes sorted
 // top-k key lists: *lists_per_query lists of k keys per query,
 // lists[(b * lists_per_query + l) * k + i].
+// gid_map (optional): global id of row r is gid_map[r] instead of gid_offset + r.
 remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc, int k, float sigma,
-                       const float* xnorm, int64_t n_rows, int64_t gid_offset, uint64_t* cand_buf,
-                       unsigned long long* gthr, uint64_t* lists, cudaStream_t st, int* launches,
-                       int* lists_per_query);
+                       const float* xnorm, int64_t n_rows, int64_t gid_offset, const int64_t* gid_map,
+                       uint64_t* cand_buf, unsigned long long* gthr, uint64_t* lists, cudaStream_t st,
+                       int* launches, int* lists_per_query);
 // Largest lists_per_query tc_scan can produce (workspace sizing).
-constexpr int kTcMaxStatesPerCta = 1;
-constexpr int kTcEpilogueThreads = 128;
+constexpr int kTcMaxStatesPerCta = 2;
+constexpr int kTcEpilogueThreads = 256;
 
 }  // namespace remoe
