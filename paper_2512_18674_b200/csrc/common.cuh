@@ -95,9 +95,11 @@ __device__ __forceinline__ uint64_t warp_key_at(const uint64_t (&v)[P], int pos)
 
 // Sort the first `cnt` keys of buf (others read as 0) and write the best `k`
 // back to buf[0..k) (or to `out` if non-null).  Returns the k-th best key
-// (0 if cnt < k).  Whole warp, warp-uniform arguments.
+// (0 if cnt < k).  Whole warp, warp-uniform arguments.  Out of line: one copy of
+// the unrolled network per kernel keeps the instruction footprint small (a cold
+// instruction cache, not the sort, dominated small merges when it was inlined).
 template <int P>
-__device__ __forceinline__ uint64_t warp_compact(uint64_t* buf, int cnt, int k, uint64_t* out) {
+__device__ __noinline__ uint64_t warp_compact(uint64_t* buf, int cnt, int k, uint64_t* out) {
   const int lane = threadIdx.x & 31;
   uint64_t v[P];
 #pragma unroll

@@ -1,0 +1,33 @@
+// host_util.h -- host helpers shared by the kernel launchers.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <set>
+#include <utility>
+
+namespace remoe {
+
+// Kernel attributes (max dynamic shared memory, carveout) are per function and per
+// device; set them once per (function, device) instead of on every launch.
+inline cudaError_t set_smem_attrs_once(const void* fn, int max_dyn_smem) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({fn, dev})) return cudaSuccess;
+  if (max_dyn_smem > 0) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn_smem);
+    if (e != cudaSuccess) return e;
+  }
+  // the same (maximal) shared-memory carveout for every SPS kernel: consecutive kernels
+  // of a query never force an SM reconfiguration
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e != cudaSuccess) return e;
+  done.insert({fn, dev});
+  return cudaSuccess;
+}
+
+}  // namespace remoe

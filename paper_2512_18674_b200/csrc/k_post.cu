@@ -2,6 +2,7 @@
 //   S0/S1 row norms, S4/S5 key-list merge, S6+S7 softmax + gather + weighted
 //   reduce, the multi-GPU winner-row gather, S8 expert plan, build validation.
 #include "common.cuh"
+#include "host_util.h"
 #include "kernels.h"
 
 namespace remoe {
@@ -35,110 +36,233 @@ cudaError_t launch_norms(const uint16_t* x, int64_t n, int dim, float* out, cuda
   if (n <= 0) return cudaSuccess;
   const int wpb = 8;
   const int64_t grid = (n + wpb - 1) / wpb;
+  cudaError_t e = set_smem_attrs_once((const void*)k_norms, 0);
+  if (e != cudaSuccess) return e;
   k_norms<<<(unsigned)grid, wpb * 32, 0, st>>>(x, n, dim, out, zero_u64, zero_stride);
   return cudaGetLastError();
 }
 
+__device__ __forceinline__ void finalize_query(const uint64_t* tb, int k, int b, const FinalizeArgs& f,
+                                               int64_t j0, int64_t j1, bool write_ids);
+
 // ---------------------------------------------------------------- S4 / S5 merge
-// One CTA per query: 8 warps each keep a warp-shared top-k over a subset of the
-// lists, then warp 0 merges the 8 partial results.  Exact.
-template <int P>
+// One CTA per query.  The answer is the k largest keys of the union of the lists
+// (keys are unique: they carry the global id).  Exact selection:
+//   1. every warp streams whole lists (4 loads in flight), and keys >= lb -- a known
+//      lower bound of the final k-th key (the scan's shared threshold; 1 = "any real
+//      key") -- are appended to shared memory with one atomic per warp;
+//   2. n <= kRankMax survivors: each survivor's rank = #{survivors > it} (broadcast
+//      reads of shared memory, O(n^2 / 256) compares per thread), rank < k -> out[rank];
+//      kRankMax < n <= kSelCap: block bitonic sort; n > kSelCap: an MSB-first 8-bit
+//      radix select finds the k-th largest key T exactly, and keys >= T are re-collected.
+constexpr int kSelCap = 2048;
+constexpr int kRankMax = 512;
+
+__device__ __forceinline__ void block_sort_desc(uint64_t* a, int np2) {
+  for (int size = 2; size <= np2; size <<= 1) {
+    for (int j = size >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < (np2 >> 1); i += blockDim.x) {
+        const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1)), hi = lo + j;  // j is a power of 2
+        const uint64_t x = a[lo], y = a[hi];
+        const bool desc = (lo & size) == 0;
+        if (desc ? x < y : x > y) { a[lo] = y; a[hi] = x; }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, int n_lists,
                                                int64_t qstride, int64_t lstride, int k,
                                                uint64_t* __restrict__ out,
-                                               unsigned long long* __restrict__ set_thr) {
-  constexpr int CAP = 32 * P;
-  extern __shared__ __align__(16) uint64_t msm[];
-  uint64_t* buf = msm;               // [8][CAP]
-  uint64_t* part = msm + 8 * CAP;    // [8][k]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+                                               unsigned long long* __restrict__ set_thr,
+                                               const unsigned long long* __restrict__ lower,
+                                               FinalizeArgs fin) {
+  __shared__ uint64_t cand[kSelCap];
+  __shared__ uint64_t topk[256];
+  __shared__ unsigned hist[256];
+  __shared__ int cnt;
+  __shared__ uint64_t prefix_s;
+  __shared__ int need_s;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int b = blockIdx.x;
   const uint64_t* base = in + (int64_t)b * qstride;
-  WarpTopk<P> tk;
-  tk.init(buf + warp * CAP);
-  for (int l = warp; l < n_lists; l += 8) {
-    const uint64_t* li = base + (int64_t)l * lstride;
-    for (int i0 = 0; i0 < k; i0 += 32) {
-      const uint64_t key = (i0 + lane < k) ? li[i0 + lane] : 0ull;
-      // lists are sorted descending: once a chunk has nothing above the
-      // threshold, the rest of the list cannot contribute either
-      if (!__any_sync(kFull, key > tk.thr)) break;
-      tk.push(key, k);
+  const int nch = (k + 31) >> 5;
+  const int items = n_lists * nch;
+  uint64_t lb = lower ? lower[b] : 0ull;
+  if (lb == 0) lb = 1;  // sentinel keys (0) never count
+  auto item_key = [&](int it) -> uint64_t {
+    if (it >= items) return 0ull;
+    const int l = nch == 1 ? it : it / nch, c = it - l * nch;
+    const int i = c * 32 + lane;
+    return i < k ? __ldg(base + (int64_t)l * lstride + i) : 0ull;
+  };
+  auto collect = [&](uint64_t thr_lo) {  // append keys >= thr_lo to cand (warp-aggregated)
+    for (int it0 = warp; it0 < items; it0 += 8 * 4) {
+      uint64_t kk[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) kk[u] = item_key(it0 + 8 * u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const unsigned m = __ballot_sync(kFull, kk[u] >= thr_lo);
+        if (m) {
+          int pos0 = 0;
+          if (lane == 0) pos0 = atomicAdd(&cnt, __popc(m));
+          pos0 = __shfl_sync(kFull, pos0, 0);
+          const int pos = pos0 + __popc(m & ((1u << lane) - 1u));
+          if (kk[u] >= thr_lo && pos < kSelCap) cand[pos] = kk[u];
+        }
+      }
     }
+  };
+  // Lists are sorted: the k-th largest list head is a real key <= the final k-th key,
+  // a much tighter bound than lb when the state lists are many (S4: 2 per CTA).
+  if (n_lists >= k && n_lists <= kSelCap) {
+    if (t == 0) prefix_s = 0ull;
+    for (int l = t; l < n_lists; l += blockDim.x) cand[l] = __ldg(base + (int64_t)l * lstride);
+    __syncthreads();
+    for (int i = t; i < n_lists; i += blockDim.x) {
+      const uint64_t x = cand[i];
+      if (x == 0) continue;  // empty list; real keys are distinct
+      int r = 0;
+      for (int j = 0; j < n_lists; ++j) r += cand[j] > x;
+      if (r == k - 1) prefix_s = x;
+    }
+    __syncthreads();
+    if (prefix_s > lb) lb = prefix_s;
+    __syncthreads();
   }
-  tk.finish(part + warp * k, k);
+  if (t == 0) cnt = 0;
   __syncthreads();
-  if (warp == 0) {
-    tk.init(buf);
-    for (int w = 0; w < 8; ++w)
-      for (int i0 = 0; i0 < k; i0 += 32) {
-        const uint64_t key = (i0 + lane < k) ? part[w * k + i0 + lane] : 0ull;
-        tk.push(key, k);
+  collect(lb);
+  __syncthreads();
+  int n = cnt;
+  if (n > kSelCap) {
+    // radix select of the k-th largest key among keys >= lb
+    uint64_t prefix = 0, pmask = 0;
+    int need = k;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      hist[t] = 0;
+      __syncthreads();
+      for (int it0 = warp; it0 < items; it0 += 8) {
+        const uint64_t key = item_key(it0);
+        if (key >= lb && (key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
       }
-    tk.finish(out + (int64_t)b * k, k);
-    if (set_thr) {
-      // seeding: the k-th best key of a subset of rows, minus one (strict lower bound,
-      // the subset's own rows stay admissible in the full scan)
-      __syncwarp();
-      if (lane == 0) {
-        const uint64_t kth = out[(int64_t)b * k + k - 1];
-        set_thr[b] = kth ? kth - 1 : 0ull;
+      __syncthreads();
+      if (warp == 0) {  // suffix sums over the 256 bins: lane l owns bins 255-8l .. 248-8l
+        int h[8], tot = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { h[u] = hist[255 - 8 * lane - u]; tot += h[u]; }
+        int incl = tot;  // inclusive prefix over lanes (higher bins first)
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int o = __shfl_up_sync(kFull, incl, off);
+          if (lane >= off) incl += o;
+        }
+        int c = incl - tot;  // keys in higher bins than this lane's
+        const bool mine = c < need && incl >= need;
+        if (mine) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (c + h[u] >= need) {
+              prefix_s = prefix | ((uint64_t)(255 - 8 * lane - u) << shift);
+              need_s = need - c;
+              break;
+            }
+            c += h[u];
+          }
+        }
       }
+      __syncthreads();
+      prefix = prefix_s;
+      need = need_s;
+      pmask |= (uint64_t)255 << shift;
+      __syncthreads();
     }
+    if (t == 0) cnt = 0;
+    __syncthreads();
+    collect(prefix);  // exactly k keys: keys are unique and prefix is the k-th largest
+    __syncthreads();
+    n = cnt;
   }
-}
-
-template <int P>
-static cudaError_t merge_t(const uint64_t* in, int B, int n_lists, int64_t qstride, int64_t lstride,
-                           int k, uint64_t* out, unsigned long long* set_thr, cudaStream_t st) {
-  const size_t smem = (size_t)8 * (32 * P + k) * sizeof(uint64_t);
-  cudaError_t e = cudaFuncSetAttribute(k_merge<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k_merge<P><<<B, 256, smem, st>>>(in, n_lists, qstride, lstride, k, out, set_thr);
-  return cudaGetLastError();
+  const int nout = n < k ? n : k;
+  if (n <= kRankMax) {
+    for (int i = t; i < n; i += blockDim.x) {
+      const uint64_t x = cand[i];
+      int r = 0;
+      for (int j = 0; j < n; ++j) r += cand[j] > x;
+      if (r < k) topk[r] = x;
+    }
+  } else {
+    int np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    for (int i = n + t; i < np2; i += blockDim.x) cand[i] = 0ull;
+    __syncthreads();
+    block_sort_desc(cand, np2);
+    for (int i = t; i < nout; i += blockDim.x) topk[i] = cand[i];
+  }
+  __syncthreads();
+  for (int i = t; i < k; i += blockDim.x) out[(int64_t)b * k + i] = i < nout ? topk[i] : 0ull;
+  if (set_thr && t == 0) {
+    // seeding: the k-th best key of a subset of rows, minus one (strict lower bound,
+    // the subset's own rows stay admissible in the full scan)
+    const uint64_t kth = k <= nout ? topk[k - 1] : 0ull;
+    set_thr[b] = kth ? kth - 1 : 0ull;
+  }
+  if (fin.act != nullptr || fin.rows != nullptr) {  // fused S6 + S7 (world == 1)
+    if (nout < k)
+      for (int i = nout + t; i < k; i += blockDim.x) topk[i] = 0ull;
+    __syncthreads();
+    finalize_query(topk, k, b, fin, 0, fin.LE, true);
+  }
 }
 
 cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride, int64_t lstride,
-                         int k, uint64_t* out, cudaStream_t st, unsigned long long* set_thr) {
+                         int k, uint64_t* out, cudaStream_t st, unsigned long long* set_thr,
+                         const unsigned long long* lower, const FinalizeArgs* fin) {
   if (B <= 0) return cudaSuccess;
-  switch (topk_P(k)) {  // WarpTopk needs CAP = 32*P >= k + 32: topk_P guarantees it
-    case 2: return merge_t<2>(in, B, n_lists, qstride, lstride, k, out, set_thr, st);
-    case 4: return merge_t<4>(in, B, n_lists, qstride, lstride, k, out, set_thr, st);
-    case 8: return merge_t<8>(in, B, n_lists, qstride, lstride, k, out, set_thr, st);
-    case 16: return merge_t<16>(in, B, n_lists, qstride, lstride, k, out, set_thr, st);
-    case 32: return merge_t<32>(in, B, n_lists, qstride, lstride, k, out, set_thr, st);
-  }
-  return cudaErrorInvalidValue;
+  if (k > 256) return cudaErrorInvalidValue;
+  FinalizeArgs f{};
+  if (fin) f = *fin;
+  cudaError_t e = set_smem_attrs_once((const void*)k_merge, 0);
+  if (e != cudaSuccess) return e;
+  k_merge<<<B, 256, 0, st>>>(in, n_lists, qstride, lstride, k, out, set_thr, lower, f);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- S6 + S7
 // w_r = softmax(s_r / T), max-subtracted: s_0 is the largest score of the
 // sorted list.  exp in parallel, the normaliser by a fixed xor tree (order
 // independent of batch position).  P[e] = sum_r w_r A_r[e], r ascending.
-__global__ void __launch_bounds__(256) k_finalize(const uint64_t* __restrict__ top, int k,
-                                                  const float* __restrict__ act, int64_t offset,
-                                                  const float* __restrict__ rows, int mode,
-                                                  int64_t LE, float T, int64_t* __restrict__ ids,
-                                                  float* __restrict__ scores,
-                                                  float* __restrict__ pred) {
+// Whole CTA (256 threads); outputs j = j0 + t, j0 + t + 256, ... < j1.
+__device__ __forceinline__ void finalize_query(const uint64_t* tb, int k, int b, const FinalizeArgs& f,
+                                               int64_t j0, int64_t j1, bool write_ids) {
   __shared__ float w[256];
   __shared__ const float* src[256];
   __shared__ float red[8];
-  const int b = blockIdx.x;
   const int t = threadIdx.x;
-  const uint64_t* tb = top + (int64_t)b * k;
   const float s0 = key_score(tb[0]);
   float e = 0.f;
   if (t < k) {
     const uint64_t key = tb[t];
-    const float s = key_score(key);
-    const int64_t gid = key_gid(key);
-    ids[(int64_t)b * k + t] = gid;
-    scores[(int64_t)b * k + t] = s;
-    e = expf(__fdiv_rn(s - s0, T));
-    src[t] = mode == 0 ? act + (gid - offset) * LE : rows + ((int64_t)b * k + t) * LE;
+    if (key != 0) {
+      const float s = key_score(key);
+      const int64_t gid = key_gid(key);
+      if (write_ids) {
+        f.ids[(int64_t)b * k + t] = gid;
+        f.scores[(int64_t)b * k + t] = s;
+      }
+      e = expf(__fdiv_rn(s - s0, f.T));
+      src[t] = f.mode == 0 ? f.act + (gid - f.offset) * f.LE : f.rows + ((int64_t)b * k + t) * f.LE;
+    } else {  // fewer than k candidates (cannot happen for k <= N_total): empty slot
+      if (write_ids) {
+        f.ids[(int64_t)b * k + t] = -1;
+        f.scores[(int64_t)b * k + t] = -__int_as_float(0x7f800000);
+      }
+      src[t] = f.mode == 0 ? f.act : f.rows;  // weight 0
+    }
   }
-  if (pred == nullptr) return;
+  if (f.pred == nullptr) return;
   float z = e;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(kFull, z, off);
@@ -149,12 +273,39 @@ __global__ void __launch_bounds__(256) k_finalize(const uint64_t* __restrict__ t
   for (int i = 0; i < 8; ++i) Z += red[i];
   if (t < k) w[t] = __fdiv_rn(e, Z);
   __syncthreads();
-  float* pb = pred + (int64_t)b * LE;
-  for (int64_t j = t; j < LE; j += blockDim.x) {
-    float acc = 0.f;
-    for (int r = 0; r < k; ++r) acc = __fmaf_rn(w[r], src[r][j], acc);
-    pb[j] = acc;
+  // two outputs per thread per step, 8 rows at a time: 16 independent loads in flight
+  for (int64_t ja = j0 + t; ja < j1; ja += 2 * (int64_t)blockDim.x) {
+    const int64_t jb = ja + blockDim.x;
+    const bool vb = jb < j1;
+    float acc_a = 0.f, acc_b = 0.f;
+    for (int r0 = 0; r0 < k; r0 += 8) {
+      float xa[8], xb[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool vr = r0 + u < k;
+        xa[u] = vr ? __ldg(src[r0 + u] + ja) : 0.f;
+        xb[u] = (vr && vb) ? __ldg(src[r0 + u] + jb) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (r0 + u < k) {  // r ascending
+          acc_a = __fmaf_rn(w[r0 + u], xa[u], acc_a);
+          acc_b = __fmaf_rn(w[r0 + u], xb[u], acc_b);
+        }
+      }
+    }
+    f.pred[(int64_t)b * f.LE + ja] = acc_a;
+    if (vb) f.pred[(int64_t)b * f.LE + jb] = acc_b;
   }
+}
+
+// Grid (B, ceil(LE / 256)): every CTA recomputes its query's k weights (k <= 256
+// exps, cheap) and produces 256 outputs; chunk 0 also writes ids and scores.
+__global__ void __launch_bounds__(256) k_finalize(const uint64_t* __restrict__ top, int k, FinalizeArgs f) {
+  const int b = blockIdx.x;
+  const int64_t j0 = (int64_t)blockIdx.y * blockDim.x;
+  finalize_query(top + (int64_t)b * k, k, b, f, j0, j0 + blockDim.x < f.LE ? j0 + blockDim.x : f.LE,
+                 blockIdx.y == 0);
 }
 
 cudaError_t launch_finalize(const uint64_t* top, int B, int k, const float* act, int64_t offset,
@@ -162,7 +313,11 @@ cudaError_t launch_finalize(const uint64_t* top, int B, int k, const float* act,
                             int64_t* ids, float* scores, float* pred, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
   if (k > 256) return cudaErrorInvalidValue;
-  k_finalize<<<B, 256, 0, st>>>(top, k, act, offset, rows, mode, LE, temperature, ids, scores, pred);
+  const FinalizeArgs f{act, offset, rows, mode, LE, temperature, ids, scores, pred};
+  const unsigned chunks = pred ? (unsigned)((LE + 255) / 256) : 1u;
+  cudaError_t e = set_smem_attrs_once((const void*)k_finalize, 0);
+  if (e != cudaSuccess) return e;
+  k_finalize<<<dim3((unsigned)B, chunks), 256, 0, st>>>(top, k, f);
   return cudaGetLastError();
 }
 

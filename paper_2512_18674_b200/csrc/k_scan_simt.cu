@@ -17,6 +17,7 @@
 //     common.cuh): one 64-bit compare per score against a register threshold;
 //   * warp 9 lane 0 is the TMA producer.
 #include "common.cuh"
+#include "host_util.h"
 #include "kernels.h"
 
 namespace remoe {
@@ -185,7 +186,7 @@ size_t simt_smem_bytes(int BQ, int dim, int stage_rows, int n_stages_ring) {
 template <int BQ, int P>
 static cudaError_t launch_t(const SimtScanParams& p, int grid, size_t smem, cudaStream_t st) {
   auto kern = k_scan_simt<BQ, P>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_smem_attrs_once((const void*)kern, 232448);
   if (e != cudaSuccess) return e;
   kern<<<grid, kThreads, smem, st>>>(p);
   return cudaGetLastError();

@@ -26,6 +26,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "host_util.h"
 #include "kernels.h"
 #include "tc_host.h"
 
@@ -442,7 +443,7 @@ static cudaError_t launch_tc_t(const TcPlan* t, const TcArgs& a, cudaStream_t st
   const size_t smem = tc_smem(M, a.dim, a.n_stages, a.smem_bufs ? kTcEpilogueThreads * 32 * P * 8 : 0);
   static_assert(P >= 0, "P");
   auto kern = k_scan_tc<M, P, KR>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_smem_attrs_once((const void*)kern, kMaxSmem);
   if (e != cudaSuccess) return e;
   kern<<<t->grid, kThreads, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(t->tmap_x), a);
   return cudaGetLastError();
@@ -456,6 +457,7 @@ static cudaError_t launch_tc_m(const TcPlan* t, const TcArgs& a, cudaStream_t st
   if (a.k <= 4) return launch_tc_t<M, 0, 4>(t, a, st);
   if (a.k <= 8) return launch_tc_t<M, 0, 8>(t, a, st);
   if (a.k <= 16) return launch_tc_t<M, 0, 16>(t, a, st);
+  if (a.k <= 32) return launch_tc_t<M, 0, 32>(t, a, st);
   switch (topk_P(a.k)) {
     case 2: return launch_tc_t<M, 2>(t, a, st);
     case 4: return launch_tc_t<M, 4>(t, a, st);
@@ -474,8 +476,8 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
   // M = 128 when the 128-query slab still leaves >= 4 stages, else 64.  Candidate
   // buffers go to shared memory when that still leaves >= 4 stages.
   const int M = tc_stages(128, t->dim, 0) >= 4 ? 128 : 64;
-  const int buf_bytes = k <= 16 ? 0 : kTcEpilogueThreads * 32 * topk_P(k) * 8;
-  const bool smem_bufs = k > 16 && tc_stages(M, t->dim, buf_bytes) >= 4 && !getenv("REMOE_TC_GLOBAL_BUFS");
+  const int buf_bytes = k <= 32 ? 0 : kTcEpilogueThreads * 32 * topk_P(k) * 8;
+  const bool smem_bufs = k > 32 && tc_stages(M, t->dim, buf_bytes) >= 4 && !getenv("REMOE_TC_GLOBAL_BUFS");
   int nst = tc_stages(M, t->dim, smem_bufs ? buf_bytes : 0);
   if (const char* e = getenv("REMOE_TC_STAGES")) { const int v = atoi(e); if (v >= 2 && v < nst) nst = v; }
   *lists_per_query = t->grid * 2;

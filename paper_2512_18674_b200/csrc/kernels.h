@@ -35,14 +35,30 @@ cudaError_t launch_scan_simt(const SimtScanParams& p, int BQ, int grid, cudaStre
 cudaError_t launch_norms(const uint16_t* x, int64_t n, int dim, float* out, cudaStream_t st,
                          unsigned long long* zero_u64 = nullptr, int64_t zero_stride = 0);
 
-// S4 / S5: per query, merge n_lists sorted key lists of length k into the best k.
-// key(b, l, i) = in[b * qstride + l * lstride + i].  If set_thr is non-null, also
-// set_thr[b] = (k-th best key) - 1 (threshold seeding from a row sample).
-cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride, int64_t lstride,
-                         int k, uint64_t* out, cudaStream_t st, unsigned long long* set_thr = nullptr);
-
-// S6 + S7.  mode 0: rows come from the local table act[(gid - offset) * LE];
+// S6 + S7 arguments.  mode 0: rows come from the local table act[(gid - offset) * LE];
 // mode 1: rows come from rows[(b * k + r) * LE] (multi-GPU gathered winners).
+struct FinalizeArgs {
+  const float* act;
+  int64_t offset;
+  const float* rows;
+  int mode;
+  int64_t LE;
+  float T;
+  int64_t* ids;
+  float* scores;
+  float* pred;  // may be null: ids and scores only
+};
+
+// S4 / S5: per query, merge n_lists sorted key lists of length k into the best k.
+// key(b, l, i) = in[b * qstride + l * lstride + i].  Keys below lower[b] (a known lower
+// bound of the final k-th best key) are dropped.  If set_thr is non-null, also
+// set_thr[b] = (k-th best key) - 1 (threshold seeding from a row sample).  If fin is
+// non-null the same CTA then runs S6 + S7 for the query (fused finalize).
+cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride, int64_t lstride,
+                         int k, uint64_t* out, cudaStream_t st, unsigned long long* set_thr = nullptr,
+                         const unsigned long long* lower = nullptr, const FinalizeArgs* fin = nullptr);
+
+// S6 + S7 as a separate kernel (multi-GPU path, after the row exchange).
 cudaError_t launch_finalize(const uint64_t* top, int B, int k, const float* act, int64_t offset,
                             const float* rows, int mode, int64_t LE, float temperature,
                             int64_t* ids, float* scores, float* pred, cudaStream_t st);

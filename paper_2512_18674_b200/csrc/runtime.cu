@@ -418,29 +418,37 @@ static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k
   CUDA_TRY(h->prof_mark(st, false));
   ++h->prof_launches;  // one S2+S3 phase per query chunk
   h->last_kernel = which;
-  // ---- S4
-  uint64_t* top = h->local_top;
-  CUDA_TRY(remoe::launch_merge(h->lists, bc, grid, (int64_t)grid * k, k, k, h->local_top, st));
+  // ---- S4 (+ S5..S7 fused when world == 1).  gthr[b] holds a lower bound of the
+  // final k-th best key (every published value is some state's own k-th best or a
+  // seeded strict bound), so the merge drops every key below it.
+  const remoe::FinalizeArgs fin_local{h->act, c.global_offset, nullptr, 0, h->LE, c.temperature,
+                                      ids, scores, pred};
+  if (c.world == 1) {
+    CUDA_TRY(remoe::launch_merge(h->lists, bc, grid, (int64_t)grid * k, k, k, h->local_top, st, nullptr,
+                                 h->gthr, &fin_local));
+    ++*launches;
+    return REMOE_OK;
+  }
+  CUDA_TRY(remoe::launch_merge(h->lists, bc, grid, (int64_t)grid * k, k, k, h->local_top, st, nullptr,
+                               h->gthr));
   ++*launches;
-  // ---- S5
-  if (c.world > 1) {
-    NCCL_TRY(ncclAllGather(h->local_top, h->gathered, (size_t)bc * k, ncclUint64, h->comm, st));
-    CUDA_TRY(remoe::launch_merge(h->gathered, bc, c.world, k, (int64_t)bc * k, k, h->global_top, st));
+  // ---- S5: every rank gathers all ranks' local top-k keys and runs the same merge
+  NCCL_TRY(ncclAllGather(h->local_top, h->gathered, (size_t)bc * k, ncclUint64, h->comm, st));
+  if (!pred) {
+    CUDA_TRY(remoe::launch_merge(h->gathered, bc, c.world, k, (int64_t)bc * k, k, h->global_top, st, nullptr,
+                                 nullptr, &fin_local));
     ++*launches;
-    top = h->global_top;
+    return REMOE_OK;
   }
-  // ---- S6 + S7
-  if (pred && c.world > 1) {
-    CUDA_TRY(remoe::launch_gather_rows(top, bc, k, h->act, c.global_offset, c.n_local, h->LE, h->rows, st));
-    NCCL_TRY(ncclAllReduce(h->rows, h->rows, (size_t)bc * k * h->LE, ncclFloat, ncclSum, h->comm, st));
-    CUDA_TRY(remoe::launch_finalize(top, bc, k, h->act, c.global_offset, h->rows, 1, h->LE,
-                                    c.temperature, ids, scores, pred, st));
-    *launches += 2;
-  } else {
-    CUDA_TRY(remoe::launch_finalize(top, bc, k, h->act, c.global_offset, nullptr, 0, h->LE,
-                                    c.temperature, ids, scores, pred, st));
-    ++*launches;
-  }
+  CUDA_TRY(remoe::launch_merge(h->gathered, bc, c.world, k, (int64_t)bc * k, k, h->global_top, st));
+  // ---- S6 + S7: owners contribute their winner rows (zeros elsewhere); one exact
+  // all-reduce gives every rank every winner row, then the same r-ascending sum
+  CUDA_TRY(remoe::launch_gather_rows(h->global_top, bc, k, h->act, c.global_offset, c.n_local, h->LE,
+                                     h->rows, st));
+  NCCL_TRY(ncclAllReduce(h->rows, h->rows, (size_t)bc * k * h->LE, ncclFloat, ncclSum, h->comm, st));
+  CUDA_TRY(remoe::launch_finalize(h->global_top, bc, k, h->act, c.global_offset, h->rows, 1, h->LE,
+                                  c.temperature, ids, scores, pred, st));
+  *launches += 3;
   return REMOE_OK;
 }
 
