@@ -313,6 +313,13 @@ struct WarpTopk {
   }
 };
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Wait until the previous kernel on the stream has completed and its writes are
+// visible (no-op when the kernel was not launched with PDL).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Allow the next (PDL-launched) kernel to be scheduled before this one completes.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- mbarrier + bulk copy
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

@@ -30,4 +30,23 @@ inline cudaError_t set_smem_attrs_once(const void* fn, int max_dyn_smem) {
   return cudaSuccess;
 }
 
+// Launch with Programmatic Dependent Launch: the kernel may start while the previous
+// kernel on the stream is still finishing; it must execute griddepcontrol.wait before
+// touching that kernel's outputs (see pdl_wait / pdl_trigger in common.cuh).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 }  // namespace remoe

@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
   __shared__ int need_s;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int b = blockIdx.x;
+  pdl_wait();  // the scan's lists and thresholds
   const uint64_t* base = in + (int64_t)b * qstride;
   const int nch = (k + 31) >> 5;
   const int items = n_lists * nch;
@@ -226,8 +227,8 @@ cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride
   if (fin) f = *fin;
   cudaError_t e = set_smem_attrs_once((const void*)k_merge, 0);
   if (e != cudaSuccess) return e;
-  k_merge<<<B, 256, 0, st>>>(in, n_lists, qstride, lstride, k, out, set_thr, lower, f);
-  return cudaGetLastError();
+  return launch_pdl(k_merge, dim3(B), dim3(256), 0, st, in, n_lists, qstride, lstride, k, out, set_thr,
+                    lower, f);
 }
 
 // ---------------------------------------------------------------- S6 + S7

@@ -111,6 +111,7 @@ struct TcArgs {
   uint64_t* out;
   int smem_bufs;  // candidate buffers in shared memory (else cand_buf in global memory)
   const int64_t* gid_map;  // global id of row r = gid_map[r] if non-null, else gid_offset + r
+  int merge_in_cta;        // register top-k: merge the two parity states into one list per CTA
 };
 }  // namespace
 
@@ -138,6 +139,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t n_tiles = (p.n_rows + kTileN - 1) / kTileN;
+  pdl_trigger();  // the merge kernel may be scheduled as SMs free up
 
   // ---- one-time setup: barriers, TMEM, the resident query slab
   if (threadIdx.x == 0) {
@@ -240,6 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int parity = e >> 2;
     const int m = (M == 128) ? quarter * 32 + lane : quarter * 16 + lane;
     const bool active = (M == 128 || lane < 16) && m < p.nq;
+    pdl_wait();  // k_norms: query norms and zeroed shared thresholds
     const float qn = active ? p.qnorm[m] : 0.f;
     const int slot = e * 32 + lane;
     float* xs = sXn + e * kTileN;  // this warp's copy of the tile's |x_j|
@@ -370,10 +373,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if constexpr (KR > 0) tk.publish();
     }
-    uint64_t* out =
-        active ? p.out + (((size_t)m * gridDim.x + blockIdx.x) * 2 + parity) * (size_t)p.k : nullptr;
-    if constexpr (KR > 0) tk.flush(out);
-    else tk.flush(out, p.k);
+    if (KR > 0 && p.merge_in_cta) {
+      // Merge the two parity states of each query inside the CTA (one list per CTA per
+      // query halves the merge kernel's input).  The TMA stage ring is idle now (every
+      // tile has been consumed), so it serves as scratch: state (slot) -> KR keys.
+      uint64_t* scratch = reinterpret_cast<uint64_t*>(sB);
+      // every epilogue warp has consumed its last accumulator, so every MMA has completed
+      // and every TMA load has landed: only then is the ring free
+      asm volatile("bar.sync 2, %0;" ::"n"(kEpiWarps * 32) : "memory");
+      if constexpr (KR > 0) tk.flush(scratch + (size_t)slot * KR);  // all KR slots (k <= KR)
+      asm volatile("bar.sync %0, 64;" ::"r"(3 + quarter) : "memory");  // the quarter's two warps
+      if (parity == 0 && active) {
+        const uint64_t* a = scratch + (size_t)slot * (KR > 0 ? KR : 1);
+        const uint64_t* b = scratch + (size_t)(slot + 128) * (KR > 0 ? KR : 1);  // warp e + 4, same lane
+        uint64_t* o = p.out + ((size_t)m * gridDim.x + blockIdx.x) * (size_t)p.k;
+        int ia = 0, ib = 0;
+        for (int r = 0; r < p.k; ++r) {  // two-pointer merge of two descending lists
+          const uint64_t x = a[ia], y = b[ib];
+          if (x >= y) { o[r] = x; ++ia; } else { o[r] = y; ++ib; }
+        }
+      }
+    } else {
+      uint64_t* out =
+          active ? p.out + (((size_t)m * gridDim.x + blockIdx.x) * 2 + parity) * (size_t)p.k : nullptr;
+      if constexpr (KR > 0) tk.flush(out);
+      else tk.flush(out, p.k);
+    }
   }
   __syncthreads();
   if (warp == 1) {
@@ -445,8 +470,10 @@ static cudaError_t launch_tc_t(const TcPlan* t, const TcArgs& a, cudaStream_t st
   auto kern = k_scan_tc<M, P, KR>;
   cudaError_t e = set_smem_attrs_once((const void*)kern, kMaxSmem);
   if (e != cudaSuccess) return e;
-  kern<<<t->grid, kThreads, smem, st>>>(*reinterpret_cast<const CUtensorMap*>(t->tmap_x), a);
-  return cudaGetLastError();
+  // PDL: the prologue (barriers, TMEM, query slab, first TMA loads) overlaps the tail of
+  // k_norms; the epilogue waits for it (query norms, zeroed thresholds)
+  return launch_pdl(kern, dim3(t->grid), dim3(kThreads), smem, st,
+                    *reinterpret_cast<const CUtensorMap*>(t->tmap_x), a);
 }
 
 template <int M>
@@ -480,7 +507,11 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
   const bool smem_bufs = k > 32 && tc_stages(M, t->dim, buf_bytes) >= 4 && !getenv("REMOE_TC_GLOBAL_BUFS");
   int nst = tc_stages(M, t->dim, smem_bufs ? buf_bytes : 0);
   if (const char* e = getenv("REMOE_TC_STAGES")) { const int v = atoi(e); if (v >= 2 && v < nst) nst = v; }
-  *lists_per_query = t->grid * 2;
+  // register top-k merges its two parity states in-CTA when the stage ring can hold them
+  const int KR = k <= 1 ? 1 : k <= 2 ? 2 : k <= 4 ? 4 : k <= 8 ? 8 : k <= 16 ? 16 : 32;
+  const bool in_cta = k <= 32 && (size_t)nst * kStageBytes >= (size_t)kTcEpilogueThreads * KR * 8;
+  const int lists_per_cta = in_cta ? 1 : 2;
+  *lists_per_query = t->grid * lists_per_cta;
   for (int s0 = 0; s0 < bc; s0 += M) {
     TcArgs a{};
     a.xnorm = xnorm;
@@ -496,7 +527,8 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
     a.cand_buf = cand_buf;
     a.gthr = gthr + s0;
     a.gid_map = gid_map;
-    a.out = lists + (size_t)s0 * t->grid * 2 * k;
+    a.out = lists + (size_t)s0 * t->grid * lists_per_cta * k;
+    a.merge_in_cta = in_cta ? 1 : 0;
     a.smem_bufs = smem_bufs ? 1 : 0;
     cudaError_t e = (M == 128) ? launch_tc_m<128>(t, a, st) : launch_tc_m<64>(t, a, st);
     if (e != cudaSuccess) return REMOE_ERR_CUDA;
