@@ -140,6 +140,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x & 31;
   const int64_t n_tiles = (p.n_rows + kTileN - 1) / kTileN;
   pdl_trigger();  // the merge kernel may be scheduled as SMs free up
+  // Query slab of this CTA (blockIdx.y).  With several slabs, the CTAs of every slab walk
+  // the store tiles in the same order (tile = blockIdx.x + j * gridDim.x), so the slabs
+  // read each tile at about the same time: HBM once, the other slabs hit L2.
+  const int slab = blockIdx.y;
+  const int nq = min(M, p.nq - slab * M);
+  const uint16_t* qsl = p.q + (size_t)slab * M * D;
+  const float* qnorm_sl = p.qnorm + slab * M;
+  unsigned long long* gthr_sl = p.gthr + slab * M;
+  const int lists_per_cta = p.merge_in_cta ? 1 : 2;
+  uint64_t* out_sl = p.out + (size_t)slab * M * gridDim.x * lists_per_cta * p.k;
+  const size_t cta_lin = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
 
   // ---- one-time setup: barriers, TMEM, the resident query slab
   if (threadIdx.x == 0) {
@@ -168,8 +179,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int cc = i - m * (D / 8);
       const int kb = cc >> 3, c = cc & 7;
       const uint32_t dst = a_s + (uint32_t)(kb * M * 128 + m * 128 + ((c ^ (m & 7)) << 4));
-      const uint16_t* src = p.q + (size_t)(m < p.nq ? m : 0) * D + cc * 8;
-      const uint32_t bytes = m < p.nq ? 16u : 0u;  // src-size 0 -> zero fill
+      const uint16_t* src = qsl + (size_t)(m < nq ? m : 0) * D + cc * 8;
+      const uint32_t bytes = m < nq ? 16u : 0u;  // src-size 0 -> zero fill
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes)
                    : "memory");
     }
@@ -241,19 +252,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     const int parity = e >> 2;
     const int m = (M == 128) ? quarter * 32 + lane : quarter * 16 + lane;
-    const bool active = (M == 128 || lane < 16) && m < p.nq;
+    const bool active = (M == 128 || lane < 16) && m < nq;
     pdl_wait();  // k_norms: query norms and zeroed shared thresholds
-    const float qn = active ? p.qnorm[m] : 0.f;
+    const float qn = active ? qnorm_sl[m] : 0.f;
     const int slot = e * 32 + lane;
     float* xs = sXn + e * kTileN;  // this warp's copy of the tile's |x_j|
     constexpr int kCap = 32 * (P > 0 ? P : 2);
     uint64_t* buf = p.smem_bufs ? sBuf + (size_t)slot * kCap
-                                : p.cand_buf + ((size_t)blockIdx.x * kTcEpilogueThreads + slot) * kCap;
+                                : p.cand_buf + (cta_lin * kTcEpilogueThreads + slot) * kCap;
     // KR > 0: register top-KR (k <= KR <= 16); otherwise buffer + compaction (any k <= 256)
     using Topk = typename std::conditional<(KR > 0), RegTopk<(KR > 0 ? KR : 1)>, LaneTopk<(P > 0 ? P : 2)>>::type;
     Topk tk;
-    if constexpr (KR > 0) tk.init(p.k, active ? p.gthr + m : nullptr);
-    else tk.init(buf, active ? p.gthr + m : nullptr);
+    if constexpr (KR > 0) tk.init(p.k, active ? gthr_sl + m : nullptr);
+    else tk.init(buf, active ? gthr_sl + m : nullptr);
     if (!active) tk.tlim = __int_as_float(0x7f800000);  // +inf: never a candidate
     // the tile's |x_j| (lane l loads rows 4l..4l+3) are loaded one tile ahead
     auto load_xn = [&](int64_t t) {
@@ -386,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (parity == 0 && active) {
         const uint64_t* a = scratch + (size_t)slot * (KR > 0 ? KR : 1);
         const uint64_t* b = scratch + (size_t)(slot + 128) * (KR > 0 ? KR : 1);  // warp e + 4, same lane
-        uint64_t* o = p.out + ((size_t)m * gridDim.x + blockIdx.x) * (size_t)p.k;
+        uint64_t* o = out_sl + ((size_t)m * gridDim.x + blockIdx.x) * (size_t)p.k;
         int ia = 0, ib = 0;
         for (int r = 0; r < p.k; ++r) {  // two-pointer merge of two descending lists
           const uint64_t x = a[ia], y = b[ib];
@@ -395,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     } else {
       uint64_t* out =
-          active ? p.out + (((size_t)m * gridDim.x + blockIdx.x) * 2 + parity) * (size_t)p.k : nullptr;
+          active ? out_sl + (((size_t)m * gridDim.x + blockIdx.x) * 2 + parity) * (size_t)p.k : nullptr;
       if constexpr (KR > 0) tk.flush(out);
       else tk.flush(out, p.k);
     }
@@ -464,7 +475,7 @@ remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int 
 void tc_plan_destroy(TcPlan* t) { t->ok = false; }
 
 template <int M, int P, int KR = 0>
-static cudaError_t launch_tc_t(const TcPlan* t, const TcArgs& a, cudaStream_t st) {
+static cudaError_t launch_tc_t(const TcPlan* t, const TcArgs& a, dim3 grid, cudaStream_t st) {
   const size_t smem = tc_smem(M, a.dim, a.n_stages, a.smem_bufs ? kTcEpilogueThreads * 32 * P * 8 : 0);
   static_assert(P >= 0, "P");
   auto kern = k_scan_tc<M, P, KR>;
@@ -472,25 +483,25 @@ static cudaError_t launch_tc_t(const TcPlan* t, const TcArgs& a, cudaStream_t st
   if (e != cudaSuccess) return e;
   // PDL: the prologue (barriers, TMEM, query slab, first TMA loads) overlaps the tail of
   // k_norms; the epilogue waits for it (query norms, zeroed thresholds)
-  return launch_pdl(kern, dim3(t->grid), dim3(kThreads), smem, st,
+  return launch_pdl(kern, grid, dim3(kThreads), smem, st,
                     *reinterpret_cast<const CUtensorMap*>(t->tmap_x), a);
 }
 
 template <int M>
-static cudaError_t launch_tc_m(const TcPlan* t, const TcArgs& a, cudaStream_t st) {
-  // register top-k for k <= 16 (list length pow2ceil(k))
-  if (a.k <= 1) return launch_tc_t<M, 0, 1>(t, a, st);
-  if (a.k <= 2) return launch_tc_t<M, 0, 2>(t, a, st);
-  if (a.k <= 4) return launch_tc_t<M, 0, 4>(t, a, st);
-  if (a.k <= 8) return launch_tc_t<M, 0, 8>(t, a, st);
-  if (a.k <= 16) return launch_tc_t<M, 0, 16>(t, a, st);
-  if (a.k <= 32) return launch_tc_t<M, 0, 32>(t, a, st);
+static cudaError_t launch_tc_m(const TcPlan* t, const TcArgs& a, dim3 g, cudaStream_t st) {
+  // register top-k for k <= 32 (list length pow2ceil(k))
+  if (a.k <= 1) return launch_tc_t<M, 0, 1>(t, a, g, st);
+  if (a.k <= 2) return launch_tc_t<M, 0, 2>(t, a, g, st);
+  if (a.k <= 4) return launch_tc_t<M, 0, 4>(t, a, g, st);
+  if (a.k <= 8) return launch_tc_t<M, 0, 8>(t, a, g, st);
+  if (a.k <= 16) return launch_tc_t<M, 0, 16>(t, a, g, st);
+  if (a.k <= 32) return launch_tc_t<M, 0, 32>(t, a, g, st);
   switch (topk_P(a.k)) {
-    case 2: return launch_tc_t<M, 2>(t, a, st);
-    case 4: return launch_tc_t<M, 4>(t, a, st);
-    case 8: return launch_tc_t<M, 8>(t, a, st);
-    case 16: return launch_tc_t<M, 16>(t, a, st);
-    case 32: return launch_tc_t<M, 32>(t, a, st);
+    case 2: return launch_tc_t<M, 2>(t, a, g, st);
+    case 4: return launch_tc_t<M, 4>(t, a, g, st);
+    case 8: return launch_tc_t<M, 8>(t, a, g, st);
+    case 16: return launch_tc_t<M, 16>(t, a, g, st);
+    case 32: return launch_tc_t<M, 32>(t, a, g, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -511,8 +522,15 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
   const int KR = k <= 1 ? 1 : k <= 2 ? 2 : k <= 4 ? 4 : k <= 8 ? 8 : k <= 16 ? 16 : 32;
   const bool in_cta = k <= 32 && (size_t)nst * kStageBytes >= (size_t)kTcEpilogueThreads * KR * 8;
   const int lists_per_cta = in_cta ? 1 : 2;
-  *lists_per_query = t->grid * lists_per_cta;
-  for (int s0 = 0; s0 < bc; s0 += M) {
+  // Query slabs of M: one launch covers up to grid slabs, each slab on grid / slabs CTAs
+  // walking the store in the same tile order (L2 sharing of every tile across slabs).
+  const int n_slabs = (bc + M - 1) / M;
+  const int slabs_per_launch = n_slabs < t->grid ? n_slabs : t->grid;
+  const int ctas_per_slab = t->grid / slabs_per_launch;
+  *lists_per_query = ctas_per_slab * lists_per_cta;
+  for (int sl0 = 0; sl0 < n_slabs; sl0 += slabs_per_launch) {
+    const int ns = n_slabs - sl0 < slabs_per_launch ? n_slabs - sl0 : slabs_per_launch;
+    const int s0 = sl0 * M;
     TcArgs a{};
     a.xnorm = xnorm;
     a.n_rows = n_rows;
@@ -520,17 +538,18 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
     a.dim = t->dim;
     a.q = q + (size_t)s0 * t->dim;
     a.qnorm = qnorm + s0;
-    a.nq = bc - s0 < M ? bc - s0 : M;
+    a.nq = bc - s0;  // queries of this launch; slab y takes [y*M, y*M + M)
     a.k = k;
     a.sigma = sigma;
     a.n_stages = nst;
     a.cand_buf = cand_buf;
     a.gthr = gthr + s0;
     a.gid_map = gid_map;
-    a.out = lists + (size_t)s0 * t->grid * lists_per_cta * k;
+    a.out = lists + (size_t)s0 * ctas_per_slab * lists_per_cta * k;
     a.merge_in_cta = in_cta ? 1 : 0;
     a.smem_bufs = smem_bufs ? 1 : 0;
-    cudaError_t e = (M == 128) ? launch_tc_m<128>(t, a, st) : launch_tc_m<64>(t, a, st);
+    const dim3 g((unsigned)ctas_per_slab, (unsigned)ns);
+    cudaError_t e = (M == 128) ? launch_tc_m<128>(t, a, g, st) : launch_tc_m<64>(t, a, g, st);
     if (e != cudaSuccess) return REMOE_ERR_CUDA;
     ++*launches;
   }
