@@ -21,6 +21,7 @@
 // The dot for (q, row) accumulates K-blocks in ascending order inside the tensor core;
 // it does not depend on the query's batch position, on M, or on the sharding.
 #include <cuda.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <type_traits>
@@ -57,6 +58,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// Multicast variant: the box lands at the same offset in every CTA of cta_mask and
+// completes tx bytes on each destination CTA's mbarrier at the same offset.
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, int c0, int c1,
+                                               uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(cta_mask)
+      : "memory");
+}
+
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
                                           uint32_t accumulate) {
   asm volatile(
@@ -70,6 +82,16 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
                : "memory");
+}
+
+// Arrive (when this thread's prior MMAs complete) on the mbarrier at the same offset in
+// every CTA of cta_mask.
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(cta_mask)
+      : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_before() {
@@ -112,6 +134,7 @@ struct TcArgs {
   int smem_bufs;  // candidate buffers in shared memory (else cand_buf in global memory)
   const int64_t* gid_map;  // global id of row r = gid_map[r] if non-null, else gid_offset + r
   int merge_in_cta;        // register top-k: merge the two parity states into one list per CTA
+  int cluster;             // CTAs per cluster along y (multicast of the store tiles), 1 = none
 };
 }  // namespace
 
@@ -132,8 +155,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = bars + NST;
   uint64_t* tfull = bars + 2 * NST;
   uint64_t* tempty = bars + 2 * NST + kAcc;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NST + 2 * kAcc);
-  float* sXn = reinterpret_cast<float*>(bars + 2 * NST + 2 * kAcc + 2);  // [8 warps][128] x-norms
+  uint64_t* cempty = bars + 2 * NST + 2 * kAcc;  // [NST] cluster-wide "slot free" (leader CTA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NST + 2 * kAcc);
+  // [8 warps][128] x-norms, 16-byte aligned for ld/st.shared.v4
+  float* sXn = reinterpret_cast<float*>(bars + ((3 * NST + 2 * kAcc + 2 + 1) & ~1));
   uint64_t* sBuf = reinterpret_cast<uint64_t*>(sXn + kEpiWarps * kTileN);  // [256][CAP] if p.smem_bufs
 
   const int warp = threadIdx.x >> 5;
@@ -152,12 +177,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* out_sl = p.out + (size_t)slab * M * gridDim.x * lists_per_cta * p.k;
   const size_t cta_lin = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
 
+  // Cluster of C = p.cluster CTAs along y (consecutive slabs, same tile sequence): the
+  // leader (rank 0) multicasts every store tile into all C CTAs' shared memory, so one
+  // L2 read feeds C query slabs.  Every CTA's MMA commit frees the slot in its own ring
+  // (empty: pacing its expect_tx) and in the leader's (cempty, count C: pacing the load).
+  const int C = p.cluster;
+  uint32_t crank = 0;
+  if (C > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+
   // ---- one-time setup: barriers, TMEM, the resident query slab
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&cempty[s], C);
+    }
     for (int s = 0; s < kAcc; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_x) : "memory");
+  }
+  if (C > 1) {  // every CTA's barriers exist before any peer multicasts or arrives
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -197,9 +237,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % NST;
           const uint32_t ph = (uint32_t)(it / NST) & 1u;
-          mbar_wait(&empty[s], ph ^ 1u);
+          mbar_wait(&empty[s], ph ^ 1u);  // this CTA's MMA is done with the slot
           mbar_arrive_expect_tx(&full[s], kStageBytes);
-          tma_load_2d(sB + (size_t)s * kStageBytes, &tmap_x, kb * kBlockK, (int)(t * kTileN), &full[s]);
+          if (C == 1) {
+            tma_load_2d(sB + (size_t)s * kStageBytes, &tmap_x, kb * kBlockK, (int)(t * kTileN), &full[s]);
+          } else if (crank == 0) {
+            mbar_wait(&cempty[s], ph ^ 1u);  // every CTA of the cluster is done with the slot
+            tma_load_2d_mc(sB + (size_t)s * kStageBytes, &tmap_x, kb * kBlockK, (int)(t * kTileN), &full[s],
+                           (uint16_t)((1u << C) - 1u));
+          }
         }
       }
     }
@@ -230,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma_bf16(d_tmem, umma_desc(abase + kk * 32), umma_desc(bbase + kk * 32), idesc,
                       (kb | kk) != 0);
           umma_commit(&empty[s]);
+          if (C > 1) umma_commit_mc(&cempty[s], 1);  // the leader's slot-free barrier
         }
         umma_commit(&tfull[acc]);
       }
@@ -297,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       xv_next = load_xn(t + tstep);
       gt_next = tk.peek_shared();
-      mbar_wait(&tfull[acc], aph);
+      mbar_wait_sleep(&tfull[acc], aph);
       if (active) tk.raise(gt);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kTileN);
@@ -412,6 +459,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   __syncthreads();
+  if (C > 1) {  // no CTA leaves while a peer may still arrive on its barriers
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemCols));
@@ -422,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 static size_t tc_smem(int M, int D, int nst, int buf_bytes) {
   return 1024 + (size_t)(D / kBlockK) * M * 128 + (size_t)nst * kStageBytes +
-         (2 * (size_t)nst + 2 * kAcc + 2) * 8 + kEpiWarps * kTileN * 4 + (size_t)buf_bytes;
+         (3 * (size_t)nst + 2 * kAcc + 4) * 8 + kEpiWarps * kTileN * 4 + (size_t)buf_bytes;
 }
 
 static int tc_stages(int M, int D, int buf_bytes) {
@@ -481,8 +531,25 @@ static cudaError_t launch_tc_t(const TcPlan* t, const TcArgs& a, dim3 grid, cuda
   auto kern = k_scan_tc<M, P, KR>;
   cudaError_t e = set_smem_attrs_once((const void*)kern, kMaxSmem);
   if (e != cudaSuccess) return e;
+  if (a.cluster > 1) {
+    // largest cluster size (<= requested) that divides the slabs and keeps every cluster
+    // co-resident (tiles are assigned statically: a second wave would double the time)
+    TcArgs& aa = const_cast<TcArgs&>(a);
+    while (aa.cluster > 1 && ((grid.y % aa.cluster) != 0 ||
+                              (int)(grid.x * grid.y / aa.cluster) >
+                                  max_active_clusters((const void*)kern, dim3(kThreads), smem, aa.cluster)))
+      aa.cluster >>= 1;
+    if (getenv("REMOE_VERBOSE"))
+      fprintf(stderr, "[remoe] tc scan grid (%u,%u) cluster %d (max active clusters of 8/4/2: %d/%d/%d)\n",
+              grid.x, grid.y, aa.cluster, max_active_clusters((const void*)kern, dim3(kThreads), smem, 8),
+              max_active_clusters((const void*)kern, dim3(kThreads), smem, 4),
+              max_active_clusters((const void*)kern, dim3(kThreads), smem, 2));
+  }
   // PDL: the prologue (barriers, TMEM, query slab, first TMA loads) overlaps the tail of
   // k_norms; the epilogue waits for it (query norms, zeroed thresholds)
+  if (a.cluster > 1)
+    return launch_pdl_cluster(kern, grid, dim3(kThreads), smem, st, (unsigned)a.cluster,
+                              *reinterpret_cast<const CUtensorMap*>(t->tmap_x), a);
   return launch_pdl(kern, grid, dim3(kThreads), smem, st,
                     *reinterpret_cast<const CUtensorMap*>(t->tmap_x), a);
 }
@@ -548,6 +615,7 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
     a.out = lists + (size_t)s0 * ctas_per_slab * lists_per_cta * k;
     a.merge_in_cta = in_cta ? 1 : 0;
     a.smem_bufs = smem_bufs ? 1 : 0;
+    a.cluster = getenv("REMOE_NO_MULTICAST") ? 1 : 8;  // reduced to what fits in launch_tc_t
     const dim3 g((unsigned)ctas_per_slab, (unsigned)ns);
     cudaError_t e = (M == 128) ? launch_tc_m<128>(t, a, g, st) : launch_tc_m<64>(t, a, g, st);
     if (e != cudaSuccess) return REMOE_ERR_CUDA;
