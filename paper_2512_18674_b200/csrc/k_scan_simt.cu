@@ -25,7 +25,7 @@ namespace remoe {
 namespace {
 constexpr int kComputeWarps = 8;
 constexpr int kThreads = (kComputeWarps + 2) * 32;
-constexpr int kRB = 2;  // rows per compute step per warp
+constexpr int kRB = 4;  // rows per compute step per warp
 }  // namespace
 
 template <int BQ, int P>
@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan_simt(SimtScanParams p) {
       float* Sb = S + sb * SR * BQ;
       mbar_wait(&full[st], ph);
       mbar_wait(&sempty[sb], sph ^ 1u);
+      const uint32_t stg_s = smem_u32(stg), qs_s = smem_u32(qs);
       for (int i = warp * kRB; i < rows; i += kComputeWarps * kRB) {
         float acc[kRB][BQ];
 #pragma unroll
@@ -93,7 +94,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan_simt(SimtScanParams p) {
 #pragma unroll
           for (int r = 0; r < kRB; ++r) {
             uint4 w = make_uint4(0, 0, 0, 0);
-            if (i + r < rows) w = lds128(stg + ((size_t)(i + r) * D + (size_t)c * 8) * 2);
+            if (i + r < rows)
+              asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                           : "r"(stg_s + (uint32_t)(((i + r) * D + c * 8) * 2)));
             xf[r][0] = bf_lo(w.x); xf[r][1] = bf_hi(w.x);
             xf[r][2] = bf_lo(w.y); xf[r][3] = bf_hi(w.y);
             xf[r][4] = bf_lo(w.z); xf[r][5] = bf_hi(w.z);
@@ -101,8 +105,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan_simt(SimtScanParams p) {
           }
 #pragma unroll
           for (int b = 0; b < BQ; ++b) {
-            const float4 qa = lds128f(qs + (size_t)b * D + c * 8);
-            const float4 qb = lds128f(qs + (size_t)b * D + c * 8 + 4);
+            float4 qa, qb;
+            const uint32_t qaddr = qs_s + (uint32_t)((b * D + c * 8) * 4);
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                         : "=f"(qa.x), "=f"(qa.y), "=f"(qa.z), "=f"(qa.w) : "r"(qaddr));
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                         : "=f"(qb.x), "=f"(qb.y), "=f"(qb.z), "=f"(qb.w) : "r"(qaddr + 16));
 #pragma unroll
             for (int r = 0; r < kRB; ++r) {
               float a = acc[r][b];
@@ -121,15 +129,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_scan_simt(SimtScanParams p) {
           for (int r = 0; r < kRB; ++r)
 #pragma unroll
             for (int b = 0; b < BQ; ++b) acc[r][b] += __shfl_xor_sync(kFull, acc[r][b], off);
+        // lane j < kRB*BQ computes the score of (row j / BQ, query j % BQ): one division
+        // per lane, all in parallel
+        float mine = 0.f;
 #pragma unroll
-        for (int r = 0; r < kRB; ++r) {
-          if (i + r < rows) {
-            const float xn = p.xnorm[rbase + i + r];
+        for (int r = 0; r < kRB; ++r)
 #pragma unroll
-            for (int b = 0; b < BQ; ++b)
-              if (lane == r * BQ + b) Sb[(i + r) * BQ + b] = eq11(acc[r][b], qn[b], xn, p.sigma);
-          }
-        }
+          for (int b = 0; b < BQ; ++b)
+            if (lane == r * BQ + b) mine = acc[r][b];
+        const int rr = lane / BQ, bb = lane % BQ;
+        if (lane < kRB * BQ && i + rr < rows)
+          Sb[(i + rr) * BQ + bb] = eq11(mine, qn[bb], __ldg(p.xnorm + rbase + i + rr), p.sigma);
       }
       __syncwarp();
       if (lane == 0) { mbar_arrive(&empty[st]); mbar_arrive(&sfull[sb]); }

@@ -294,7 +294,7 @@ static remoe_status_t build_impl(remoe_sps* h, const uint16_t* emb, const float*
 
   // ---- kernel geometry + workspaces
   h->grid_simt = h->num_sms;
-  h->stage_rows = std::max(1, std::min(64, 32768 / (2 * c.dim)));
+  h->stage_rows = std::max(1, std::min(64, 65536 / (2 * c.dim)));  // 64 KB TMA stages
   const int capmax = 32 * remoe::topk_P(c.max_k);
   ST_TRY(remoe::tc_plan_create(&h->tc, h->x, c.n_local, c.dim, h->num_sms, c.max_k));
   h->grid_tc = h->tc.grid;
@@ -384,7 +384,7 @@ static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k
   if (which == 1) {
     grid = h->grid_simt;
     const int BQ = bc >= 8 ? 8 : bc >= 4 ? 4 : bc >= 2 ? 2 : 1;
-    const int NST = std::max(2, std::min(6, (int)((200 * 1024 - (size_t)BQ * c.dim * 4) /
+    const int NST = std::max(2, std::min(6, (int)((210 * 1024 - (size_t)BQ * c.dim * 4) /
                                                    ((size_t)h->stage_rows * c.dim * 2))));
     for (int s0 = 0; s0 < bc; s0 += BQ) {
       remoe::SimtScanParams p{};
