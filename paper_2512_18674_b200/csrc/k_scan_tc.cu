@@ -135,6 +135,7 @@ struct TcArgs {
   const int64_t* gid_map;  // global id of row r = gid_map[r] if non-null, else gid_offset + r
   int merge_in_cta;        // register top-k: merge the two parity states into one list per CTA
   int cluster;             // CTAs per cluster along y (multicast of the store tiles), 1 = none
+  int epi_sleep;           // epilogue waits with a suspend-time hint (REMOE_EPI_SLEEP=1)
 };
 }  // namespace
 
@@ -344,7 +345,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       xv_next = load_xn(t + tstep);
       gt_next = tk.peek_shared();
-      mbar_wait_sleep(&tfull[acc], aph);
+      if (p.epi_sleep) mbar_wait_sleep(&tfull[acc], aph);
+      else mbar_wait(&tfull[acc], aph);
       if (active) tk.raise(gt);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kTileN);
@@ -616,6 +618,7 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
     a.merge_in_cta = in_cta ? 1 : 0;
     a.smem_bufs = smem_bufs ? 1 : 0;
     a.cluster = getenv("REMOE_NO_MULTICAST") ? 1 : 8;  // reduced to what fits in launch_tc_t
+    a.epi_sleep = getenv("REMOE_EPI_SLEEP") ? atoi(getenv("REMOE_EPI_SLEEP")) : 0;
     const dim3 g((unsigned)ctas_per_slab, (unsigned)ns);
     cudaError_t e = (M == 128) ? launch_tc_m<128>(t, a, g, st) : launch_tc_m<64>(t, a, g, st);
     if (e != cudaSuccess) return REMOE_ERR_CUDA;
