@@ -147,3 +147,25 @@ def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
     u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
     u = u + 0x7FFF + ((u >> 16) & 1)
     return (u >> 16).astype(np.uint16)
+
+
+def token_prompts(seed: int, n_prompts: int, dim: int, min_len: int = 1, max_len: int = 64,
+                  n_topics: int = 8, zero_token_every: int = 0):
+    """Synthetic token-embedding matrices for the Eq. 11 front end (NEXT-N1).
+
+    Prompt p draws a topic; its tokens are topic centroid + unit noise, so prompts of a
+    topic have high SCS.  Returns (tokens bf16 bits [T, dim], offsets int64 [P+1], topic [P]).
+    Host-only numpy (PCG64 seeded): inputs, no method arithmetic."""
+    rng = np.random.default_rng(seed)
+    cent = rng.standard_normal((n_topics, dim))
+    lens = rng.integers(min_len, max_len + 1, size=n_prompts)
+    topic = rng.integers(0, n_topics, size=n_prompts)
+    offsets = np.zeros(n_prompts + 1, np.int64)
+    offsets[1:] = np.cumsum(lens)
+    tok = np.empty((int(offsets[-1]), dim), np.float32)
+    for p in range(n_prompts):
+        a, b = offsets[p], offsets[p + 1]
+        tok[a:b] = cent[topic[p]] + rng.standard_normal((b - a, dim))
+    if zero_token_every:
+        tok[::zero_token_every] = 0.0
+    return f32_to_bf16_bits(tok), offsets, topic

@@ -146,6 +146,34 @@ REMOE_API remoe_status_t remoe_sps_query_host(remoe_sps_t h, const uint16_t* q_b
 REMOE_API remoe_status_t remoe_expert_plan(const float* pred, int32_t B, int32_t L, int32_t E,
                                            int32_t n_cold, uint8_t* cold_mask, void* stream);
 
+/*
+ * NEXT-N1, the Eq. 11 front end: turn the pre-processing layer's
+ * token embeddings into the prompt vectors the store and the queries hold.  SCS
+ * normalises every token row and sums the rows of a prompt (V1^T X with V1 the
+ * ownership vector), so for prompt p with token rows [offsets[p], offsets[p+1]):
+ *     a_p = sum_t x_t / |x_t|      (fp32; a zero token contributes 0, DESIGN R17)
+ *   tokens_bf16: device [T x dim] bf16 bits, T = offsets[n_prompts];
+ *   offsets:     device [n_prompts + 1] int64, non-decreasing, offsets[0] = 0;
+ *   out_bf16:    device [n_prompts x dim] bf16 (round to nearest even), or NULL;
+ *   out_f32:     device [n_prompts x dim] fp32, or NULL (at least one non-NULL).
+ *   dim % 8 == 0, 8 <= dim <= 4096.  Stateless; async on `stream`.
+ */
+REMOE_API remoe_status_t remoe_sps_embed(const uint16_t* tokens_bf16, const int64_t* offsets,
+                                         int32_t n_prompts, int32_t dim, uint16_t* out_bf16,
+                                         float* out_f32, void* stream);
+
+/*
+ * NEXT-N4, prediction quality: the paper scores its predictor by the
+ * Jensen-Shannon divergence between predicted and true expert-activation
+ * distributions.  out[b] = (1/L) sum_l JS_2(P[b][l][:], Q[b][l][:]), log base 2 (so
+ * 0 <= JS <= 1, DESIGN R18), 0 log 0 = 0.
+ *   P: device [B x L x E] fp32 (e.g. remoe_sps_query's pred);
+ *   Q: device [B x L x E] fp32, or one [L x E] matrix for every b if shared_q != 0;
+ *   out: device [B] fp32.  Rows are expected to be distributions (not checked).
+ */
+REMOE_API remoe_status_t remoe_js_divergence(const float* P, const float* Q, int32_t shared_q,
+                                             int32_t B, int32_t L, int32_t E, float* out, void* stream);
+
 /* Rank 0 calls this, then broadcasts the 128 bytes to all ranks (e.g. as a uint8
  * tensor over a torch.distributed group) before remoe_sps_build. */
 REMOE_API remoe_status_t remoe_nccl_unique_id(uint8_t out[128]);

@@ -43,6 +43,8 @@ def _lib():
         lib.oracle_predict.argtypes = [vp, vp, i64, vp, i64, i64, i64, vp]
         lib.oracle_plan.argtypes = [vp, i64, i32, i32, i32, vp]
         lib.oracle_widen_bf16.argtypes = [vp, i64, vp]
+        lib.oracle_js_divergence.argtypes = [vp, vp, i32, i32]
+        lib.oracle_js_divergence.restype = f64
         for f in ("oracle_sps_bf16", "oracle_sps_f64", "oracle_scores_bf16",
                   "oracle_pair_scores_bf16", "oracle_select", "oracle_softmax",
                   "oracle_predict", "oracle_plan"):
@@ -180,3 +182,14 @@ def plan(pred, n_cold) -> np.ndarray:
     if rc:
         raise ValueError("oracle_plan failed (n_cold out of range)")
     return mask
+
+
+def js_divergence(p, q) -> float:
+    """NEXT-N4: base-2 Jensen-Shannon divergence of two [L, E] activation matrices, mean over
+    layers (PAPER.md:371, P:675)."""
+    p = _c(p, np.float64)
+    q = _c(q, np.float64)
+    if p.ndim == 1:
+        p, q = p[None], q[None]
+    assert p.shape == q.shape
+    return float(_lib().oracle_js_divergence(p.ctypes.data, q.ctypes.data, p.shape[0], p.shape[1]))

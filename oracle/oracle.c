@@ -266,3 +266,21 @@ int oracle_pair_scores_bf16(const uint16_t* q_bits, const uint16_t* x_bits, int 
   free(a); free(b);
   return 0;
 }
+
+/* ---- NEXT-N4: Jensen-Shannon divergence, log base 2 ("JS Divergence of expert
+ * activation distributions", P:675 the prediction-accuracy metric; base 2 so the maximum is
+ * 1, SPEC S:247 reading), averaged over the L layer rows.  JS(p,q) = KL(p||m)/2 + KL(q||m)/2,
+ * m = (p+q)/2, with 0 log 0 = 0. */
+double oracle_js_divergence(const double* p, const double* q, int L, int E) {
+  double total = 0.0;
+  for (int l = 0; l < L; ++l) {
+    double js = 0.0;
+    for (int e = 0; e < E; ++e) {
+      const double a = p[l * E + e], b = q[l * E + e], m = 0.5 * (a + b);
+      if (a > 0.0) js += 0.5 * a * log2(a / m);
+      if (b > 0.0) js += 0.5 * b * log2(b / m);
+    }
+    total += js;
+  }
+  return total / L;
+}

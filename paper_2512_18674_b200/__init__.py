@@ -7,5 +7,5 @@ from .sps import (  # noqa: F401
     ABI_FUNCTIONS, KERNEL_AUTO, KERNEL_STREAM, KERNEL_TC, LIB_PATH, RemoeError, Sps, SpsConfig,
     SpsInfo, lib, remoe_expert_plan, remoe_nccl_unique_id, remoe_sps_build,
     remoe_sps_config_default, remoe_sps_destroy, remoe_sps_get_info, remoe_sps_profile, remoe_sps_query,
-    remoe_sps_query_host, remoe_sps_set_kernel, remoe_sps_sync,
+    remoe_sps_query_host, remoe_sps_set_kernel, remoe_sps_sync, remoe_sps_embed, embed, remoe_js_divergence, js_divergence,
 )

@@ -71,6 +71,15 @@ cudaError_t launch_gather_rows(const uint64_t* top, int B, int k, const float* a
 cudaError_t launch_plan(const float* pred, int B, int L, int E, int n_cold, uint8_t* mask,
                         cudaStream_t st);
 
+// NEXT-N1: prompt vectors a_p = sum_t x_t / |x_t| over the token rows [off[p], off[p+1]).
+cudaError_t launch_embed(const uint16_t* tok, const int64_t* off, int n_prompts, int dim, uint16_t* out_bf16,
+                         float* out_f32, cudaStream_t st);
+
+// NEXT-N4: out[b] = mean over layers of JS_2(P[b][l], Q[b][l]); Q[b] = Q + b * q_stride
+// (q_stride = 0: one reference matrix for every b).
+cudaError_t launch_js(const float* P, const float* Q, int64_t q_stride, int B, int L, int E, float* out,
+                      cudaStream_t st);
+
 // Build-time validation: counts non-finite embeddings and bad activation rows.
 cudaError_t launch_validate(const uint16_t* x, int64_t n, int dim, const float* act, int64_t LE_rows,
                             int E, unsigned long long* bad, cudaStream_t st);

@@ -518,6 +518,27 @@ remoe_status_t remoe_expert_plan(const float* pred, int32_t B, int32_t L, int32_
   return REMOE_OK;
 }
 
+remoe_status_t remoe_sps_embed(const uint16_t* tokens_bf16, const int64_t* offsets, int32_t n_prompts,
+                               int32_t dim, uint16_t* out_bf16, float* out_f32, void* stream) {
+  if (n_prompts < 0) return fail(REMOE_ERR_INVALID_ARG, "n_prompts must be >= 0");
+  if (dim < 8 || dim % 8 != 0) return fail(REMOE_ERR_INVALID_ARG, "dim must be a positive multiple of 8");
+  if (dim > 4096) return fail(REMOE_ERR_UNSUPPORTED, "dim > 4096");
+  if (n_prompts == 0) return REMOE_OK;
+  if (!offsets || (!out_bf16 && !out_f32)) return fail(REMOE_ERR_INVALID_ARG, "offsets/outputs are NULL");
+  CUDA_TRY(remoe::launch_embed(tokens_bf16, offsets, n_prompts, dim, out_bf16, out_f32, (cudaStream_t)stream));
+  return REMOE_OK;
+}
+
+remoe_status_t remoe_js_divergence(const float* P, const float* Q, int32_t shared_q, int32_t B, int32_t L,
+                                   int32_t E, float* out, void* stream) {
+  if (B < 0 || L < 1 || E < 1) return fail(REMOE_ERR_INVALID_ARG, "need B >= 0, L >= 1, E >= 1");
+  if (B == 0) return REMOE_OK;
+  if (!P || !Q || !out) return fail(REMOE_ERR_INVALID_ARG, "P/Q/out is NULL");
+  if ((int64_t)L * 4 > 200 * 1024) return fail(REMOE_ERR_UNSUPPORTED, "L too large");
+  CUDA_TRY(remoe::launch_js(P, Q, shared_q ? 0 : (int64_t)L * E, B, L, E, out, (cudaStream_t)stream));
+  return REMOE_OK;
+}
+
 remoe_status_t remoe_sps_sync(remoe_sps_t h) {
   if (!h) return fail(REMOE_ERR_STATE, "handle is NULL");
   DeviceGuard dg(h->cfg.device);

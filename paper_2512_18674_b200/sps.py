@@ -24,7 +24,7 @@ ABI_FUNCTIONS = (
     "remoe_sps_config_default", "remoe_sps_build", "remoe_sps_query", "remoe_sps_query_host",
     "remoe_expert_plan", "remoe_nccl_unique_id", "remoe_sps_sync", "remoe_sps_get_info",
     "remoe_sps_set_kernel", "remoe_sps_profile", "remoe_sps_destroy", "remoe_status_string",
-    "remoe_last_error",
+    "remoe_last_error", "remoe_sps_embed", "remoe_js_divergence",
 )
 
 
@@ -95,6 +95,8 @@ def lib():
         L.remoe_sps_set_kernel.argtypes = [vp, i32]
         L.remoe_sps_profile.argtypes = [vp, i32, ctypes.POINTER(ctypes.c_double),
                                         ctypes.POINTER(ctypes.c_int64)]
+        L.remoe_sps_embed.argtypes = [vp, vp, i32, i32, vp, vp, vp]
+        L.remoe_js_divergence.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp]
         L.remoe_sps_destroy.argtypes = [vp]
         L.remoe_sps_destroy.restype = None
         L.remoe_status_string.argtypes = [i32]
@@ -103,7 +105,8 @@ def lib():
         L.remoe_last_error.restype = ctypes.c_char_p
         for f in ("remoe_sps_build", "remoe_sps_query", "remoe_sps_query_host", "remoe_expert_plan",
                   "remoe_nccl_unique_id", "remoe_sps_sync", "remoe_sps_get_info",
-                  "remoe_sps_set_kernel", "remoe_sps_profile"):
+                  "remoe_sps_set_kernel", "remoe_sps_profile", "remoe_sps_embed",
+                  "remoe_js_divergence"):
             getattr(L, f).restype = i32
         _LIB = L
     return _LIB
@@ -195,6 +198,40 @@ def remoe_sps_profile(h: int, enable: bool) -> tuple[float, int]:
     n = ctypes.c_int64()
     _check(lib().remoe_sps_profile(h, 1 if enable else 0, ctypes.byref(ms), ctypes.byref(n)))
     return ms.value, n.value
+
+
+def remoe_sps_embed(tokens_bf16, offsets, n_prompts: int, dim: int, out_bf16=None, out_f32=None,
+                    stream=None):
+    """NEXT-N1: prompt vectors a_p = sum_t x_t / |x_t| from token embeddings (device buffers)."""
+    _check(lib().remoe_sps_embed(_ptr(tokens_bf16), _ptr(offsets), n_prompts, dim, _ptr(out_bf16),
+                                 _ptr(out_f32), _stream(stream)))
+
+
+def embed(tokens_bf16, offsets, want_f32=False, stream=None):
+    """Torch convenience: tokens [T, D] (int16/uint16 bf16 bits, CUDA), offsets [P+1] int64 (CUDA).
+    Returns (bf16 bits [P, D] as int16, fp32 [P, D] or None)."""
+    import torch
+    P = offsets.shape[0] - 1
+    D = tokens_bf16.shape[1]
+    ob = torch.empty((P, D), dtype=torch.int16, device=tokens_bf16.device)
+    of = torch.empty((P, D), dtype=torch.float32, device=tokens_bf16.device) if want_f32 else None
+    remoe_sps_embed(tokens_bf16, offsets, P, D, ob, of, stream)
+    return ob, of
+
+
+def remoe_js_divergence(P, Q, shared_q: bool, B: int, L: int, E: int, out, stream=None):
+    """NEXT-N4: out[b] = mean_l JS_2(P[b,l], Q[b,l] or Q[l]) on device buffers."""
+    _check(lib().remoe_js_divergence(_ptr(P), _ptr(Q), 1 if shared_q else 0, B, L, E, _ptr(out),
+                                     _stream(stream)))
+
+
+def js_divergence(P, Q, stream=None):
+    """Torch convenience: P [B, L, E], Q [B, L, E] or [L, E] (CUDA fp32) -> [B] fp32."""
+    import torch
+    B, L, E = P.shape
+    out = torch.empty(B, dtype=torch.float32, device=P.device)
+    remoe_js_divergence(P, Q, Q.dim() == 2, B, L, E, out, stream)
+    return out
 
 
 def remoe_sps_destroy(h: int):

@@ -244,3 +244,22 @@ def test_whole_path_vs_numpy_scipy_bruteforce():
     for i in range(7, c.batch, 8):
         np.testing.assert_array_equal(ids[i], ids[i - 1])
         np.testing.assert_array_equal(pred[i], pred[i - 1])
+
+
+# ---------------------------------------------------------------- NEXT-N4 JS divergence
+
+def test_js_divergence_pins():
+    """Identical -> 0; disjoint supports -> 1 (base-2 maximum); [.5,.5] vs [.9,.1] ->
+    0.146793 (re-derived; SPEC S:249's 0.2089 is wrong); symmetric; equals
+    scipy's jensenshannon(base=2)**2 (a library routine) row by row, averaged over layers."""
+    from scipy.spatial.distance import jensenshannon
+    assert oracle.js_divergence([[0.2, 0.3, 0.5]], [[0.2, 0.3, 0.5]]) == 0.0
+    assert abs(oracle.js_divergence([[1.0, 0.0]], [[0.0, 1.0]]) - 1.0) <= 1e-15
+    assert abs(oracle.js_divergence([[0.5, 0.5]], [[0.9, 0.1]]) - 0.146793) <= 5e-7
+    rng = np.random.default_rng(9)
+    for L, E in [(1, 2), (3, 8), (27, 64)]:
+        p = rng.random((L, E)); p[rng.random((L, E)) < 0.2] = 0; p /= p.sum(1, keepdims=True)
+        q = rng.random((L, E)); q /= q.sum(1, keepdims=True)
+        ref = np.mean([jensenshannon(p[l], q[l], base=2) ** 2 for l in range(L)])
+        assert abs(oracle.js_divergence(p, q) - ref) <= 1e-12
+        assert abs(oracle.js_divergence(p, q) - oracle.js_divergence(q, p)) <= 1e-15
