@@ -136,6 +136,7 @@ struct TcArgs {
   int merge_in_cta;        // register top-k: merge the two parity states into one list per CTA
   int cluster;             // CTAs per cluster along y (multicast of the store tiles), 1 = none
   int epi_sleep;           // epilogue waits with a suspend-time hint (REMOE_EPI_SLEEP=1)
+  unsigned long long* stats;  // REMOE_TC_STATS: [0] candidate columns, [1] inserts, [2] chunks with a candidate
 };
 }  // namespace
 
@@ -160,7 +161,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NST + 2 * kAcc);
   // [8 warps][128] x-norms, 16-byte aligned for ld/st.shared.v4
   float* sXn = reinterpret_cast<float*>(bars + ((3 * NST + 2 * kAcc + 2 + 1) & ~1));
-  uint64_t* sBuf = reinterpret_cast<uint64_t*>(sXn + kEpiWarps * kTileN);  // [256][CAP] if p.smem_bufs
+  // [128] per-query threshold shared by the two parity states of the CTA (register top-k)
+  unsigned long long* pair_thr = reinterpret_cast<unsigned long long*>(sXn + kEpiWarps * kTileN);
+  uint64_t* sBuf = reinterpret_cast<uint64_t*>(pair_thr + 128);  // [256][CAP] if p.smem_bufs
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -194,6 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&cempty[s], C);
     }
     for (int s = 0; s < kAcc; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
+    for (int s = 0; s < 128; ++s) pair_thr[s] = 0ull;
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_x) : "memory");
   }
@@ -331,6 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     const int64_t tstep = 2 * (int64_t)gridDim.x;
     float4 xv_next = load_xn(blockIdx.x + parity * (int64_t)gridDim.x);
+    uint64_t pair_pub = 0;  // last value this state shared with its parity partner
     uint64_t gt_next = tk.peek_shared();  // shared threshold, also read one tile ahead
     int i = parity;
     for (int64_t t = blockIdx.x + parity * (int64_t)gridDim.x; t < n_tiles; t += tstep, i += 2) {
@@ -360,6 +365,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
+        if constexpr (KR > 0) {
+          // the other parity state of this query lives in the same CTA: share its k-th best
+          // through shared memory every chunk (exact: disjoint rows, own k-th best keys)
+          if (active) tk.raise(*reinterpret_cast<volatile unsigned long long*>(pair_thr + quarter * 32 + lane));
+        }
         const float* xc = xs + c * 32;
         unsigned mask = 0;
 #pragma unroll
@@ -381,14 +391,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) vl[j] = __uint_as_float(v[j]);
             const int64_t gbase = p.gid_offset + row0 + c * 32;
+            if (p.stats) {
+              atomicAdd(p.stats + 0, (unsigned long long)__popc(mask));
+              if (lane == 0) atomicAdd(p.stats + 2, 1ull);
+            }
             while (mask) {  // per lane: insertion network, no warp synchronisation
               const int j = __ffs(mask) - 1;
               mask &= mask - 1;
               const float den = __fmaf_rn(qn, xc[j], p.sigma);
               if (vl[j] >= tk.tlim * den) {
                 const int64_t gid = p.gid_map ? p.gid_map[row0 + c * 32 + j] : gbase + j;
-                tk.insert(make_key(__fdiv_rn(vl[j], den), gid));
+                const uint64_t key = make_key(__fdiv_rn(vl[j], den), gid);
+                if (p.stats && key > tk.thr) atomicAdd(p.stats + 1, 1ull);
+                tk.insert(key);
               }
+            }
+            if (active && tk.thr > pair_pub) {
+              atomicMax(pair_thr + quarter * 32 + lane, (unsigned long long)tk.thr);
+              pair_pub = tk.thr;
             }
           }
         } else {
@@ -474,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 static size_t tc_smem(int M, int D, int nst, int buf_bytes) {
   return 1024 + (size_t)(D / kBlockK) * M * 128 + (size_t)nst * kStageBytes +
-         (3 * (size_t)nst + 2 * kAcc + 4) * 8 + kEpiWarps * kTileN * 4 + (size_t)buf_bytes;
+         (3 * (size_t)nst + 2 * kAcc + 4) * 8 + kEpiWarps * kTileN * 4 + 128 * 8 + (size_t)buf_bytes;
 }
 
 static int tc_stages(int M, int D, int buf_bytes) {
@@ -619,9 +639,22 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
     a.smem_bufs = smem_bufs ? 1 : 0;
     a.cluster = getenv("REMOE_NO_MULTICAST") ? 1 : 8;  // reduced to what fits in launch_tc_t
     a.epi_sleep = getenv("REMOE_EPI_SLEEP") ? atoi(getenv("REMOE_EPI_SLEEP")) : 0;
+    static unsigned long long* stats = nullptr;
+    if (getenv("REMOE_TC_STATS")) {
+      if (!stats) { cudaMalloc(&stats, 3 * 8); }
+      cudaMemsetAsync(stats, 0, 3 * 8, st);
+      a.stats = stats;
+    }
     const dim3 g((unsigned)ctas_per_slab, (unsigned)ns);
     cudaError_t e = (M == 128) ? launch_tc_m<128>(t, a, g, st) : launch_tc_m<64>(t, a, g, st);
     if (e != cudaSuccess) return REMOE_ERR_CUDA;
+    if (a.stats) {
+      unsigned long long h[3];
+      cudaMemcpyAsync(h, a.stats, 24, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      fprintf(stderr, "[remoe] tc stats: candidates %llu inserts %llu candidate-chunks %llu (queries %d, k %d)\n",
+              h[0], h[1], h[2], a.nq, k);
+    }
     ++*launches;
   }
   return REMOE_OK;
