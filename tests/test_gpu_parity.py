@@ -295,3 +295,35 @@ def test_c3_full_size_sampled(kern):
     pick = sorted({0, 1, 3, min(B - 1, 4), min(B - 1, 6), B - 1})
     rep = compare(q[pick], x, a, c.k, ids[pick], sc[pick], pred[pick])
     assert_parity(rep)
+
+
+# ------------------------------------------------------------------ BASELINE c4 and c5 (sampled)
+
+def test_c4_full_size_sampled():
+    """BASELINE c4: 10M x 1024, Mixtral 32x8 table, k = 32, at B = 1 (single-query latency)
+    and B = 1024 (throughput), on one GPU; sampled queries checked against the oracle."""
+    c = gen.CONFIGS["c4"]
+    x = gen.store_emb(c.store_seed, c.n, c.dim)
+    a = gen.store_act(c.store_seed, c.n, c.layers, c.experts, c.moe_topk)
+    q = gen.queries(c.store_seed, c.query_seed, c.n, c.dim, 1024, mode=1)
+    s = make(x, a, max_k=32, max_batch=1024)
+    for B, pick in ((1, [0]), (1024, [4, 517, 1023])):
+        ids, sc, pred = run(s, q[:B], 32)
+        rep = compare(q[pick], x, a, 32, ids[pick], sc[pick], pred[pick])
+        assert_parity(rep)
+    s.close()
+
+
+@pytest.mark.parametrize("k", [1, 64, 128])
+def test_c5_sweep_corners_sampled(k):
+    """BASELINE c5 corners on the c3 store: B = 4096 (internal chunks of max_batch) and
+    k in {1, 64, 128}; sampled queries vs the oracle."""
+    c, x, a = store("c3")
+    q = gen.queries(c.store_seed, c.query_seed, c.n, c.dim, 4096, mode=1)
+    s = make(x, a, max_k=128, max_batch=1024)
+    ids, sc, pred = run(s, q, k)
+    pick = [0, 5, 2047, 4095]
+    assert_parity(compare(q[pick], x, a, k, ids[pick], sc[pick], pred[pick]))
+    # identical queries (i % 8 == 7 duplicates i - 1) across chunk boundaries
+    for i in (7, 1031, 4095):
+        assert np.array_equal(ids[i], ids[i - 1]) and np.array_equal(pred[i], pred[i - 1])
