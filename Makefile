@@ -14,7 +14,9 @@ LDFLAGS   := -shared -cudart static -L$(NCCL_DIR)/lib -l:libnccl.so.2 \
 
 CU_SRCS   := $(wildcard $(CSRC)/*.cu)
 CU_OBJS   := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
-CU_HDRS   := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) include/remoe.h
+CXX_SRCS  := $(wildcard $(CSRC)/*.cpp)
+CXX_OBJS  := $(patsubst $(CSRC)/%.cpp,build/%.cpp.o,$(CXX_SRCS))
+CU_HDRS   := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.h) $(wildcard include/*.h)
 
 all: cpu $(PKG)/libremoe.so
 
@@ -31,7 +33,12 @@ build/%.o: $(CSRC)/%.cu $(CU_HDRS)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c -o $@ $<
 
-$(PKG)/libremoe.so: $(CU_OBJS)
+# Host-only planner (NEXT-N3): plain C++, no device code.
+build/%.cpp.o: $(CSRC)/%.cpp $(CU_HDRS)
+	@mkdir -p build
+	$(CXX) -O2 -std=c++17 -fPIC -fvisibility=hidden -Iinclude -c -o $@ $<
+
+$(PKG)/libremoe.so: $(CU_OBJS) $(CXX_OBJS)
 	$(NVCC) $(ARCH) -o $@ $^ $(LDFLAGS)
 
 clean:

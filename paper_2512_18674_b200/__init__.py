@@ -9,3 +9,8 @@ from .sps import (  # noqa: F401
     remoe_sps_config_default, remoe_sps_destroy, remoe_sps_get_info, remoe_sps_profile, remoe_sps_query,
     remoe_sps_query_host, remoe_sps_set_kernel, remoe_sps_sync, remoe_sps_embed, embed, remoe_js_divergence, js_divergence,
 )
+from .planner import (  # noqa: F401
+    PLANNER_FUNCTIONS, remoe_convexity_threshold, remoe_fit_latency_curve, remoe_greedy_replicas,
+    remoe_lpt_partition, remoe_mmp, remoe_optimize_remote_memory, remoe_replica_time_bound,
+    remoe_worst_case_tokens,
+)

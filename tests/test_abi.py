@@ -10,10 +10,12 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "remoe.h")
+HEADERS = sorted(os.path.join(ROOT, "include", f) for f in os.listdir(os.path.join(ROOT, "include"))
+                 if f.endswith(".h"))
 
 
 def declared():
-    src = open(HEADER).read()
+    src = "".join(open(h).read() for h in HEADERS)
     return re.findall(r"REMOE_API\s+[\w\s\*]+?\b(remoe_\w+)\s*\(", src)
 
 
@@ -38,7 +40,7 @@ def test_library_exports_every_declared_symbol(lib):
     for n in declared():
         assert n in exported, n
         assert hasattr(lib, n)
-    assert set(remoe.ABI_FUNCTIONS) == set(declared())
+    assert set(remoe.ABI_FUNCTIONS) | set(remoe.PLANNER_FUNCTIONS) == set(declared())
 
 
 def test_status_strings_and_defaults(lib):
