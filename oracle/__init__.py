@@ -7,7 +7,8 @@ product path: the two share no code.  The only shared module is ``gen`` (seeded
 inputs, no method arithmetic).
 
 Parity pins live in tests/test_oracle_pins.py; every function below is pinned
-there.  Nothing here is "parity unpinned".
+there.  ``oracle.tree`` (NEXT-N2, the clustering tree and
+Algorithm 1) is pinned in tests/test_tree_oracle.py.  Nothing here is "parity unpinned".
 """
 from __future__ import annotations
 
