@@ -174,6 +174,51 @@ REMOE_API remoe_status_t remoe_sps_embed(const uint16_t* tokens_bf16, const int6
 REMOE_API remoe_status_t remoe_js_divergence(const float* P, const float* Q, int32_t shared_q,
                                              int32_t B, int32_t L, int32_t E, float* out, void* stream);
 
+/*
+ * NEXT-N2, the clustering-tree SPS (Algorithm 1) -- the paper's
+ * approximate search, next to the exact brute force of remoe_sps_query.
+ *
+ * remoe_sps_tree_build: builds the multi-fork clustering tree over this handle's store
+ * shard: every node with more than beta prompts is split by k-medoids with
+ * similarity 1 - cos (DESIGN R25), roulette-wheel centroid initialisation (R24, draws
+ * from a counter-based generator keyed by seed, node, draw) and subcluster-level
+ * centroid updates (at most max_iter updates per node; 0 keeps the initial draw).
+ * 2 <= branching <= 16, beta >= 1, beta + max_k - 1 <= 2048 (candidates per query),
+ * depth <= 63.  Synchronous; replaces a previous tree; runs on the GPU (fp64).
+ * Collective-free: with world > 1 every rank builds the tree of its own shard.
+ */
+REMOE_API remoe_status_t remoe_sps_tree_build(remoe_sps_t h, int32_t beta, int32_t branching, int32_t max_iter,
+                                              uint64_t seed);
+
+typedef struct {
+  int32_t n_nodes, n_leaves, depth, max_leaf, beta, branching;
+  double build_ms;           /* host wall time of remoe_sps_tree_build */
+} remoe_sps_tree_info_t;
+REMOE_API remoe_status_t remoe_sps_tree_info(remoe_sps_t h, remoe_sps_tree_info_t* info);
+
+/* Copies the tree to HOST buffers (each may be NULL): perm [n_local] local rows, node i
+ * owns perm[begin[i], end[i]); children child0[i] .. child0[i] + nchild[i] - 1 (nodes
+ * numbered breadth-first, root 0, parent[0] = -1); medoid[i] = local row of node i's
+ * centroid (-1 for the root).  Node arrays have remoe_sps_tree_info().n_nodes entries. */
+REMOE_API remoe_status_t remoe_sps_tree_export(remoe_sps_t h, int64_t* perm, int64_t* begin, int64_t* end,
+                                               int32_t* parent, int32_t* child0, int32_t* nchild,
+                                               int64_t* medoid);
+
+/*
+ * Algorithm 1 for B queries (same buffers and semantics as remoe_sps_query): descend by
+ * the child centroid with the best Eq. 11 key, take the leaf's prompts, supplement from
+ * sibling subtrees (best first, each explored depth-first in key order, whole leaves,
+ * climbing a level when the siblings run out) until >= k candidates (R28), return the
+ * exact top-k of the candidates by key, then the same
+ * softmax-weighted prediction (S6+S7).  leaf [B] (the leaf the descent reached) and
+ * n_eval [B] (Eq. 11 evaluations: centroids + candidates) are device outputs or NULL;
+ * with world > 1 they describe the local tree and the k winners are merged across ranks
+ * exactly as in remoe_sps_query.  REMOE_ERR_STATE before remoe_sps_tree_build.
+ */
+REMOE_API remoe_status_t remoe_sps_tree_query(remoe_sps_t h, const uint16_t* q_bf16, int32_t B, int32_t k,
+                                              int64_t* ids, float* scores, float* pred, int32_t* leaf,
+                                              int32_t* n_eval, void* stream);
+
 /* Rank 0 calls this, then broadcasts the 128 bytes to all ranks (e.g. as a uint8
  * tensor over a torch.distributed group) before remoe_sps_build. */
 REMOE_API remoe_status_t remoe_nccl_unique_id(uint8_t out[128]);

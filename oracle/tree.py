@@ -25,19 +25,21 @@ Readings (R24-R28):
       (sigma only guards Eq. 11's division; the medoid objective
       sum_{t in C} cos(x_i, x_t) is then exactly x^_i . sum_t x^_t).  Assignment: the
       most similar medoid, ties -> lower slot.  Update ("subcluster-level"): per cluster,
-      the member maximising the summed cosine to its cluster, ties -> earlier member; an
-      empty cluster keeps its medoid.  Stop when the medoids do not change or after
+      the member maximising the summed cosine to its cluster; values within
+      1e-10 * |cluster| of the maximum are ties: the current medoid stays if it is one,
+      else the earliest tied member wins; an empty cluster keeps its medoid.  Stop when the medoids do not change or after
       max_iter updates; the final assignment is to the final medoids.
   R26 children are the non-empty clusters in slot order, members in their original
       order (a stable partition of the node's range); a split with < 2 non-empty
       clusters (duplicate rows) falls back to c equal contiguous chunks.
   R27 search scores are Eq. 11 (sigma included, fp64 here); the closest child is the one
       with the larger (score, lower global id) key -- the same key order as BF.
-  R28 supplement: siblings of the current node in descending key order, each descended
-      greedily to a leaf whose members are added, until >= alpha candidates; if the
-      siblings run out, the same at the parent's level, and so on.  The answer is the
-      top-alpha by key of the gathered candidates (< alpha only if the whole walk ends
-      short: empty slots get id -1).
+  R28 supplement ("add samples into PROM until alpha samples are obtained", Alg. 1
+      line 8): the siblings of the current node in descending key order, each subtree
+      explored depth-first with children in descending key order, whole leaves added,
+      until >= alpha candidates; if the siblings run out, the same at the parent's level,
+      and so on up to the root (so alpha <= N always fills).  The answer is the
+      top-alpha by key of the gathered candidates.
 Node numbering is breadth-first (root 0, children appended in the order their parents
 split); u(seed, node, j) is the counter-based uniform below.
 """
@@ -46,6 +48,7 @@ from __future__ import annotations
 import numpy as np
 
 _M64 = (1 << 64) - 1
+TIE_TOL = 1e-10   # medoid-update tie window per member (R25)
 
 
 def splitmix64(x: int) -> int:
@@ -94,8 +97,11 @@ def assign(V: np.ndarray, m: list[int]) -> np.ndarray:
 
 
 def update(V: np.ndarray, lab: np.ndarray, m: list[int]) -> list[int]:
-    """R25: subcluster-level medoid update: argmax of the summed cosine within the cluster,
-    computed literally from the cluster's Gram matrix."""
+    """R25: subcluster-level medoid update: the member maximising the summed cosine within
+    the cluster (computed literally from the cluster's Gram matrix).  Members within
+    TIE_TOL * max(1, |cluster|) of the maximum count as maximisers: the current medoid is
+    kept if it is one, else the earliest maximiser wins (a 2-member cluster is an exact
+    tie by symmetry, so this rule is needed for a reproducible result)."""
     out = []
     for j in range(len(m)):
         idx = np.flatnonzero(lab == j)
@@ -103,7 +109,13 @@ def update(V: np.ndarray, lab: np.ndarray, m: list[int]) -> list[int]:
             out.append(m[j])
             continue
         G = V[idx] @ V[idx].T
-        out.append(int(idx[np.argmax(G.sum(axis=1))]))
+        obj = G.sum(axis=1)
+        near = obj >= obj.max() - TIE_TOL * max(1, idx.size)
+        cur = np.flatnonzero(idx == m[j])
+        if cur.size and near[cur[0]]:
+            out.append(m[j])
+        else:
+            out.append(int(idx[np.argmax(near)]))
     return out
 
 
@@ -160,10 +172,13 @@ def build_tree(x_bits: np.ndarray, beta: int, branching: int, max_iter: int, see
                 nchild=a(nchild), medoid=a(medoid))
 
 
-def _score(q: np.ndarray, qn: float, X: np.ndarray, xn: np.ndarray, rows, sigma: float) -> np.ndarray:
-    """Eq. 11 on prompt vectors, fp64 (R27)."""
+def _score(q: np.ndarray, qn: float, x_bits: np.ndarray, rows, sigma: float) -> np.ndarray:
+    """Eq. 11 on prompt vectors, fp64 (R27); widens only the rows it scores."""
+    from oracle import widen
     rows = np.asarray(rows, np.int64)
-    return (X[rows] @ q) / (qn * xn[rows] + sigma)
+    X = widen(x_bits[rows])
+    xn = np.sqrt((X * X).sum(axis=1))
+    return (X @ q) / (qn * xn + sigma)
 
 
 def _order(scores: np.ndarray, gids: np.ndarray) -> np.ndarray:
@@ -176,8 +191,7 @@ def search(tree: dict, x_bits: np.ndarray, q_bits: np.ndarray, k: int, sigma: fl
     """Algorithm 1 for every query.  Returns ids int64 [B, k], scores fp64 [B, k],
     leaf int64 [B] (the leaf the descent reached), n_eval int64 [B] (Eq. 11 evaluations)."""
     from oracle import widen
-    X = widen(np.asarray(x_bits, np.uint16))
-    xn = np.sqrt((X * X).sum(axis=1))
+    x_bits = np.asarray(x_bits, np.uint16)
     Q = widen(np.asarray(q_bits, np.uint16))
     B = Q.shape[0]
     ids = np.full((B, k), -1, np.int64)
@@ -194,7 +208,7 @@ def search(tree: dict, x_bits: np.ndarray, q_bits: np.ndarray, k: int, sigma: fl
         def ranked_children(node):
             nonlocal ne
             ch = np.arange(child0[node], child0[node] + nchild[node])
-            s = _score(q, qn, X, xn, medoid[ch], sigma)
+            s = _score(q, qn, x_bits, medoid[ch], sigma)
             ne += ch.size
             return ch[_order(s, medoid[ch] + id_offset)]
 
@@ -210,22 +224,30 @@ def search(tree: dict, x_bits: np.ndarray, q_bits: np.ndarray, k: int, sigma: fl
         leaves[bq] = leaf
         chosen = [leaf]
         count = end[leaf] - begin[leaf]
-        lvl = len(path) - 1
+
+        def explore(node):          # R28: depth-first in key order, whole leaves
+            nonlocal count
+            if nchild[node] == 0:
+                chosen.append(node)
+                count += end[node] - begin[node]
+                return
+            for c in ranked_children(node):
+                if count >= k:
+                    return
+                explore(int(c))
+
         cur = leaf
-        while count < k and lvl >= 0:       # R28
-            _, order = path[lvl]
-            for c in order:
-                if c == cur:
-                    continue
-                lf, _ = descend(int(c))
-                chosen.append(lf)
-                count += end[lf] - begin[lf]
+        for lvl in range(len(path) - 1, -1, -1):
+            if count >= k:
+                break
+            for c in path[lvl][1]:
                 if count >= k:
                     break
+                if c != cur:
+                    explore(int(c))
             cur = path[lvl][0]
-            lvl -= 1
         rows = np.concatenate([perm[begin[lf]:end[lf]] for lf in chosen])
-        s = _score(q, qn, X, xn, rows, sigma)
+        s = _score(q, qn, x_bits, rows, sigma)
         ne += rows.size
         o = _order(s, rows + id_offset)[:k]
         ids[bq, :o.size] = rows[o] + id_offset

@@ -27,6 +27,7 @@
 #include "kernels.h"
 #include "remoe.h"
 #include "tc_host.h"
+#include "tree.h"
 
 namespace {
 
@@ -117,6 +118,9 @@ struct remoe_sps {
   uint64_t* seed_top = nullptr;
   bool seed_enabled = false;  // REMOE_SEED=1: measured net-negative at small B so far
   ncclComm_t comm = nullptr;
+  // NEXT-N2 clustering tree over this shard (remoe_sps_tree_build)
+  remoe::Tree tree{};
+  bool has_tree = false;
   int force_kernel = 0;
   int last_kernel = 0;
   int last_launches = 0;
@@ -172,6 +176,7 @@ struct remoe_sps {
     prof_ev.clear();
     remoe::tc_plan_destroy(&tc);
     remoe::tc_plan_destroy(&tc_seed);
+    if (has_tree) { remoe::tree_free(&tree); has_tree = false; }
     if (comm) { ncclCommDestroy(comm); comm = nullptr; }
   }
 };
@@ -370,6 +375,40 @@ remoe_status_t remoe_sps_build(const remoe_sps_config_t* cfg, const uint16_t* em
   return s;
 }
 
+// S5..S7 from h->local_top (one sorted key list of length k per query).  world == 1:
+// S6+S7 directly; world > 1: all-gather + merge, then the owned-winner row exchange.
+static remoe_status_t post_local_top(remoe_sps* h, int bc, int k, int64_t* ids, float* scores, float* pred,
+                                     cudaStream_t st, int* launches) {
+  const remoe_sps_config_t& c = h->cfg;
+  const remoe::FinalizeArgs fin_local{h->act, c.global_offset, nullptr, 0, h->LE, c.temperature,
+                                      ids, scores, pred};
+  if (c.world == 1) {
+    CUDA_TRY(remoe::launch_finalize(h->local_top, bc, k, h->act, c.global_offset, nullptr, 0, h->LE,
+                                    c.temperature, ids, scores, pred, st));
+    ++*launches;
+    return REMOE_OK;
+  }
+  // ---- S5: every rank gathers all ranks' local top-k keys and runs the same merge
+  NCCL_TRY(ncclAllGather(h->local_top, h->gathered, (size_t)bc * k, ncclUint64, h->comm, st));
+  if (!pred) {
+    CUDA_TRY(remoe::launch_merge(h->gathered, bc, c.world, k, (int64_t)bc * k, k, h->global_top, st, nullptr,
+                                 nullptr, &fin_local));
+    ++*launches;
+    return REMOE_OK;
+  }
+  CUDA_TRY(remoe::launch_merge(h->gathered, bc, c.world, k, (int64_t)bc * k, k, h->global_top, st));
+  // ---- S6 + S7: owners contribute their winner rows (zeros elsewhere); one exact
+  // all-reduce gives every rank every winner row, then the same r-ascending sum
+  CUDA_TRY(remoe::launch_gather_rows(h->global_top, bc, k, h->act, c.global_offset, c.n_local, h->LE,
+                                     h->rows, st));
+  NCCL_TRY(ncclAllReduce(h->rows, h->rows, (size_t)bc * k * h->LE, ncclFloat, ncclSum, h->comm, st));
+  CUDA_TRY(remoe::launch_finalize(h->global_top, bc, k, h->act, c.global_offset, h->rows, 1, h->LE,
+                                  c.temperature, ids, scores, pred, st));
+  *launches += 3;
+  return REMOE_OK;
+}
+
+
 static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k, int64_t* ids,
                                   float* scores, float* pred, cudaStream_t st, int* launches) {
   const remoe_sps_config_t& c = h->cfg;
@@ -432,26 +471,8 @@ static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k
   CUDA_TRY(remoe::launch_merge(h->lists, bc, grid, (int64_t)grid * k, k, k, h->local_top, st, nullptr,
                                h->gthr));
   ++*launches;
-  // ---- S5: every rank gathers all ranks' local top-k keys and runs the same merge
-  NCCL_TRY(ncclAllGather(h->local_top, h->gathered, (size_t)bc * k, ncclUint64, h->comm, st));
-  if (!pred) {
-    CUDA_TRY(remoe::launch_merge(h->gathered, bc, c.world, k, (int64_t)bc * k, k, h->global_top, st, nullptr,
-                                 nullptr, &fin_local));
-    ++*launches;
-    return REMOE_OK;
-  }
-  CUDA_TRY(remoe::launch_merge(h->gathered, bc, c.world, k, (int64_t)bc * k, k, h->global_top, st));
-  // ---- S6 + S7: owners contribute their winner rows (zeros elsewhere); one exact
-  // all-reduce gives every rank every winner row, then the same r-ascending sum
-  CUDA_TRY(remoe::launch_gather_rows(h->global_top, bc, k, h->act, c.global_offset, c.n_local, h->LE,
-                                     h->rows, st));
-  NCCL_TRY(ncclAllReduce(h->rows, h->rows, (size_t)bc * k * h->LE, ncclFloat, ncclSum, h->comm, st));
-  CUDA_TRY(remoe::launch_finalize(h->global_top, bc, k, h->act, c.global_offset, h->rows, 1, h->LE,
-                                  c.temperature, ids, scores, pred, st));
-  *launches += 3;
-  return REMOE_OK;
+  return post_local_top(h, bc, k, ids, scores, pred, st, launches);
 }
-
 static remoe_status_t check_query(remoe_sps* h, const uint16_t* q, int32_t B, int32_t k,
                                   const int64_t* ids, const float* scores) {
   if (!h) return fail(REMOE_ERR_STATE, "handle is NULL");
@@ -503,6 +524,89 @@ remoe_status_t remoe_sps_query_host(remoe_sps_t h, const uint16_t* q, int32_t B,
                                cudaMemcpyDeviceToHost, st));
   }
   CUDA_TRY(cudaStreamSynchronize(st));
+  h->last_launches = launches;
+  return REMOE_OK;
+}
+
+// ---------------------------------------------------------------- NEXT-N2 clustering tree
+remoe_status_t remoe_sps_tree_build(remoe_sps_t h, int32_t beta, int32_t branching, int32_t max_iter,
+                                    uint64_t seed) {
+  if (!h) return fail(REMOE_ERR_STATE, "handle is NULL");
+  if (beta < 1) return fail(REMOE_ERR_INVALID_ARG, "beta must be >= 1");
+  if (branching < 2 || branching > remoe::kTreeCMax)
+    return fail(REMOE_ERR_INVALID_ARG, "branching must be in [2, %d]", remoe::kTreeCMax);
+  if (max_iter < 0) return fail(REMOE_ERR_INVALID_ARG, "max_iter must be >= 0");
+  if ((int64_t)beta + h->cfg.max_k - 1 > remoe::kTreeCandCap)
+    return fail(REMOE_ERR_UNSUPPORTED, "beta + max_k - 1 = %lld exceeds %d candidates per query",
+                (long long)beta + h->cfg.max_k - 1, remoe::kTreeCandCap);
+  DeviceGuard dg(h->cfg.device);
+  cudaStream_t st = nullptr;
+  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  remoe::Tree t;
+  std::string err;
+  const remoe_status_t s = remoe::tree_build(h->x, h->cfg.n_local, h->cfg.dim, beta, branching, max_iter, seed,
+                                             st, &t, &err);
+  cudaStreamDestroy(st);
+  if (s != REMOE_OK) return fail(s, "tree build: %s", err.c_str());
+  if (h->has_tree) remoe::tree_free(&h->tree);
+  h->tree = std::move(t);
+  h->has_tree = true;
+  return REMOE_OK;
+}
+
+remoe_status_t remoe_sps_tree_info(remoe_sps_t h, remoe_sps_tree_info_t* info) {
+  if (!h) return fail(REMOE_ERR_STATE, "handle is NULL");
+  if (!info) return fail(REMOE_ERR_INVALID_ARG, "info is NULL");
+  if (!h->has_tree) return fail(REMOE_ERR_STATE, "no tree: call remoe_sps_tree_build first");
+  const remoe::Tree& t = h->tree;
+  info->n_nodes = t.n_nodes;
+  info->n_leaves = t.n_leaves;
+  info->depth = t.depth;
+  info->max_leaf = t.max_leaf;
+  info->beta = t.beta;
+  info->branching = t.branching;
+  info->build_ms = t.build_ms;
+  return REMOE_OK;
+}
+
+remoe_status_t remoe_sps_tree_export(remoe_sps_t h, int64_t* perm, int64_t* begin, int64_t* end, int32_t* parent,
+                                     int32_t* child0, int32_t* nchild, int64_t* medoid) {
+  if (!h) return fail(REMOE_ERR_STATE, "handle is NULL");
+  if (!h->has_tree) return fail(REMOE_ERR_STATE, "no tree: call remoe_sps_tree_build first");
+  const remoe::Tree& t = h->tree;
+  DeviceGuard dg(h->cfg.device);
+  if (perm) CUDA_TRY(cudaMemcpy(perm, t.perm, (size_t)h->cfg.n_local * 8, cudaMemcpyDeviceToHost));
+  auto cp = [&](auto* dst, const auto& src) { if (dst) std::copy(src.begin(), src.end(), dst); };
+  cp(begin, t.h_begin);
+  cp(end, t.h_end);
+  cp(parent, t.h_parent);
+  cp(child0, t.h_child0);
+  cp(nchild, t.h_nchild);
+  cp(medoid, t.h_medoid);
+  return REMOE_OK;
+}
+
+remoe_status_t remoe_sps_tree_query(remoe_sps_t h, const uint16_t* q, int32_t B, int32_t k, int64_t* ids,
+                                    float* scores, float* pred, int32_t* leaf, int32_t* n_eval, void* stream) {
+  ST_TRY(check_query(h, q, B, k, ids, scores));
+  if (!h->has_tree) return fail(REMOE_ERR_STATE, "no tree: call remoe_sps_tree_build first");
+  if (B == 0) return REMOE_OK;
+  DeviceGuard dg(h->cfg.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const remoe_sps_config_t& c = h->cfg;
+  const int mb = c.max_batch;
+  int launches = 0;
+  for (int b0 = 0; b0 < B; b0 += mb) {
+    const int bc = std::min(mb, B - b0);
+    const uint16_t* qc = q + (size_t)b0 * c.dim;
+    CUDA_TRY(remoe::launch_norms(qc, bc, c.dim, h->qnorm, st));
+    CUDA_TRY(remoe::launch_tree_search(h->tree, h->x, h->xnorm, c.dim, qc, h->qnorm, bc, k, c.sigma,
+                                       c.global_offset, h->local_top, leaf ? leaf + b0 : nullptr,
+                                       n_eval ? n_eval + b0 : nullptr, st));
+    launches += 2;
+    ST_TRY(post_local_top(h, bc, k, ids + (size_t)b0 * k, scores + (size_t)b0 * k,
+                          pred ? pred + (size_t)b0 * h->LE : nullptr, st, &launches));
+  }
   h->last_launches = launches;
   return REMOE_OK;
 }

@@ -25,6 +25,7 @@ ABI_FUNCTIONS = (
     "remoe_expert_plan", "remoe_nccl_unique_id", "remoe_sps_sync", "remoe_sps_get_info",
     "remoe_sps_set_kernel", "remoe_sps_profile", "remoe_sps_destroy", "remoe_status_string",
     "remoe_last_error", "remoe_sps_embed", "remoe_js_divergence",
+    "remoe_sps_tree_build", "remoe_sps_tree_info", "remoe_sps_tree_export", "remoe_sps_tree_query",
 )
 
 
@@ -32,6 +33,18 @@ class RemoeError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{STATUS.get(status, status)}: {msg}")
         self.status = status
+
+
+class TreeInfo(ctypes.Structure):
+    _fields_ = [
+        ("n_nodes", ctypes.c_int32),
+        ("n_leaves", ctypes.c_int32),
+        ("depth", ctypes.c_int32),
+        ("max_leaf", ctypes.c_int32),
+        ("beta", ctypes.c_int32),
+        ("branching", ctypes.c_int32),
+        ("build_ms", ctypes.c_double),
+    ]
 
 
 class SpsConfig(ctypes.Structure):
@@ -97,6 +110,10 @@ def lib():
                                         ctypes.POINTER(ctypes.c_int64)]
         L.remoe_sps_embed.argtypes = [vp, vp, i32, i32, vp, vp, vp]
         L.remoe_js_divergence.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp]
+        L.remoe_sps_tree_build.argtypes = [vp, i32, i32, i32, ctypes.c_uint64]
+        L.remoe_sps_tree_info.argtypes = [vp, ctypes.POINTER(TreeInfo)]
+        L.remoe_sps_tree_export.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp]
+        L.remoe_sps_tree_query.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp]
         L.remoe_sps_destroy.argtypes = [vp]
         L.remoe_sps_destroy.restype = None
         L.remoe_status_string.argtypes = [i32]
@@ -106,7 +123,8 @@ def lib():
         for f in ("remoe_sps_build", "remoe_sps_query", "remoe_sps_query_host", "remoe_expert_plan",
                   "remoe_nccl_unique_id", "remoe_sps_sync", "remoe_sps_get_info",
                   "remoe_sps_set_kernel", "remoe_sps_profile", "remoe_sps_embed",
-                  "remoe_js_divergence"):
+                  "remoe_js_divergence", "remoe_sps_tree_build", "remoe_sps_tree_info",
+                  "remoe_sps_tree_export", "remoe_sps_tree_query"):
             getattr(L, f).restype = i32
         _LIB = L
     return _LIB
@@ -234,6 +252,35 @@ def js_divergence(P, Q, stream=None):
     return out
 
 
+def remoe_sps_tree_build(h: int, beta: int, branching: int, max_iter: int, seed: int):
+    """NEXT-N2: build the clustering tree over the handle's shard (synchronous)."""
+    _check(lib().remoe_sps_tree_build(h, beta, branching, max_iter, seed & ((1 << 64) - 1)))
+
+
+def remoe_sps_tree_info(h: int) -> TreeInfo:
+    info = TreeInfo()
+    _check(lib().remoe_sps_tree_info(h, ctypes.byref(info)))
+    return info
+
+
+def remoe_sps_tree_export(h: int, n_local: int) -> dict:
+    """The tree as numpy arrays (host copies)."""
+    n = remoe_sps_tree_info(h).n_nodes
+    out = dict(perm=np.empty(n_local, np.int64), begin=np.empty(n, np.int64), end=np.empty(n, np.int64),
+               parent=np.empty(n, np.int32), child0=np.empty(n, np.int32), nchild=np.empty(n, np.int32),
+               medoid=np.empty(n, np.int64))
+    _check(lib().remoe_sps_tree_export(h, *(out[f].ctypes.data for f in
+                                             ("perm", "begin", "end", "parent", "child0", "nchild", "medoid"))))
+    return out
+
+
+def remoe_sps_tree_query(h: int, q_bf16, B: int, k: int, ids, scores, pred=None, leaf=None, n_eval=None,
+                         stream=None):
+    """NEXT-N2: Algorithm 1 + S6/S7 on device buffers."""
+    _check(lib().remoe_sps_tree_query(h, _ptr(q_bf16), B, k, _ptr(ids), _ptr(scores), _ptr(pred), _ptr(leaf),
+                                      _ptr(n_eval), _stream(stream)))
+
+
 def remoe_sps_destroy(h: int):
     if h:
         lib().remoe_sps_destroy(h)
@@ -259,6 +306,7 @@ class Sps:
         cfg.inputs_on_device = 1 if on_dev else 0
         self.device = torch.device("cuda", device)
         self.dim, self.layers, self.experts = d, act.shape[1], act.shape[2]
+        self.n_local = n
         self.handle = remoe_sps_build(cfg, emb_bf16, act, nccl_unique_id)
 
     def query(self, q_bf16, k, want_pred=True, stream=None):
@@ -278,6 +326,30 @@ class Sps:
         pred = np.empty((B, self.layers, self.experts), np.float32) if want_pred else None
         remoe_sps_query_host(self.handle, q_bf16, B, k, ids, scores, pred, stream)
         return ids, scores, pred
+
+    def tree_build(self, beta=150, branching=8, max_iter=10, seed=0):
+        """NEXT-N2: the clustering tree; alpha = k of tree_query."""
+        remoe_sps_tree_build(self.handle, beta, branching, max_iter, seed)
+        return remoe_sps_tree_info(self.handle)
+
+    def tree_info(self) -> TreeInfo:
+        return remoe_sps_tree_info(self.handle)
+
+    def tree_export(self) -> dict:
+        return remoe_sps_tree_export(self.handle, self.n_local)
+
+    def tree_query(self, q_bf16, k, want_pred=True, stream=None):
+        """Algorithm 1: returns ids, scores, pred (or None), leaf [B], n_eval [B]."""
+        import torch
+        B = q_bf16.shape[0]
+        ids = torch.empty((B, k), dtype=torch.int64, device=self.device)
+        scores = torch.empty((B, k), dtype=torch.float32, device=self.device)
+        pred = (torch.empty((B, self.layers, self.experts), dtype=torch.float32, device=self.device)
+                if want_pred else None)
+        leaf = torch.empty(B, dtype=torch.int32, device=self.device)
+        n_eval = torch.empty(B, dtype=torch.int32, device=self.device)
+        remoe_sps_tree_query(self.handle, q_bf16, B, k, ids, scores, pred, leaf, n_eval, stream)
+        return ids, scores, pred, leaf, n_eval
 
     def plan(self, pred, n_cold, stream=None):
         import torch

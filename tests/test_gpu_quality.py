@@ -43,6 +43,10 @@ def test_sps_beats_dop_beats_ef():
     import quality
     res, pred, truth = quality.evaluate("c2", n=20_000, held_out=128, k=15)
     assert res["SPS"] < res["DOP"] < res["EF"], res
+    # NEXT-N2: the clustering tree predicts far better than DOP with a fraction of the
+    # Eq. 11 evaluations of BF ("more than 10 times faster than BF")
+    assert res["TREE"] < res["DOP"], res
+    assert res["tree"]["mean_evals"] * 10 < res["tree"]["evals_bf"], res
     # the harness's JS numbers agree with the oracle on a sample
     for i in range(0, 128, 31):
         ref = oracle.js_divergence(pred[i], truth[i])

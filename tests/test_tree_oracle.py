@@ -172,3 +172,21 @@ def test_structure_on_duplicates_fallback():
     t = T.build_tree(x, beta=10, branching=4, max_iter=5, seed=1)
     _check_structure(t, 40, 10)
     assert t["nchild"][0] == 4 and list(t["end"][1:5] - t["begin"][1:5]) == [10, 10, 10, 10]
+
+
+def test_supplement_always_fills_alpha():
+    """R28 (Alg. 1 line 8, "until alpha samples are obtained"): with alpha far above beta
+    the depth-first walk still gathers alpha distinct prompts whenever N >= alpha, and the
+    answer is the top-alpha by key of what it gathered."""
+    N, D = 900, 40
+    x = _corpus(N, D, seed=2)
+    t = T.build_tree(x, beta=20, branching=3, max_iter=25, seed=2)
+    q = gen.queries(2, 3, N, D, 40, mode=1)
+    for k in (64, 300, N):
+        ids, sc, _, ne = T.search(t, x, q, k)
+        assert np.all(ids >= 0)
+        assert all(len(set(r)) == k for r in ids)
+        assert np.all(np.diff(sc, axis=1) <= 0)
+    ids, sc, _, _ = T.search(t, x, q, N)        # alpha = N gathers everything: BF order
+    ref_ids, _, _ = oracle.sps(q, x, np.zeros((N, 1, 1), np.float32), N, want_pred=False)
+    assert np.array_equal(ids, ref_ids)
