@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--config", default="c3", choices=sorted(gen.CONFIGS))
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--k", type=int, default=None)
-    ap.add_argument("--kernel", default="auto", choices=["auto", "stream", "tc"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "stream", "tc", "pair"])
     ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
@@ -119,6 +119,12 @@ def algorithmic_bytes_per_launch(n_loc, D, nq):
     """S2 scan: the store rows + their fp32 norms + the queries of the launch
     (SURVEY §8(d) per-unit figure N_loc*(2D+4), x units = rows of the shard)."""
     return n_loc * (2 * D + 4) + nq * 2 * D
+
+
+def algorithmic_flops_per_launch(n_loc, D, nq):
+    """S2 scan: 2*D flops per (query, row) pair; the Eq. 11 scaling and the
+    top-k compare are O(1) per pair and not counted."""
+    return 2.0 * nq * n_loc * D
 
 
 def cpu_baseline(cfg, B, k, seconds, x, a):
@@ -209,7 +215,8 @@ def run_ours(args):
     else:
         sps = remoe.Sps(x, a, max_batch=max(B, 1), max_k=max(k, 1), device=local)
     if args.kernel != "auto":
-        sps.set_kernel(remoe.KERNEL_STREAM if args.kernel == "stream" else remoe.KERNEL_TC)
+        sps.set_kernel({"stream": remoe.KERNEL_STREAM, "tc": remoe.KERNEL_TC,
+                        "pair": remoe.KERNEL_PAIR}[args.kernel])
 
     # a rotating pool of distinct query batches (fresh cluster members)
     pool = 4
@@ -288,8 +295,8 @@ def run_ours(args):
     e2e_value = B * args.steps / (float(te[0]) / 1e3)
 
     info = sps.info()
-    kern = {1: "k_scan_simt (CUDA cores, TMA bulk staging)", 2: "k_scan_tc (tcgen05 + TMA)"}.get(
-        info.last_scan_kernel, "?")
+    kern = {1: "k_scan_simt (CUDA cores, TMA bulk staging)", 2: "k_scan_tc (tcgen05 + TMA)",
+            3: "k_scan_pair (tcgen05 cta_group::2 + TMA)"}.get(info.last_scan_kernel, "?")
     per_launch_ms = scan_ms_max / max(1, scan_launches)
     nq_per_launch = B / max(1, scan_launches // max(1, args.steps))
     alg = algorithmic_bytes_per_launch(n_loc, cfg.dim, nq_per_launch)
@@ -300,7 +307,11 @@ def run_ours(args):
     except OSError:
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    tc_peak = peaks.get("bf16_tflops", 2250.0)
     achieved = alg / (per_launch_ms / 1e3) / 1e9
+    flops = algorithmic_flops_per_launch(n_loc, cfg.dim, nq_per_launch)
+    # the bound: arithmetic intensity (flop per algorithmic byte, ~B) against the ridge
+    tensor_bound = flops / alg > tc_peak * 1e12 / (hbm_peak * 1e9)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -315,11 +326,20 @@ def run_ours(args):
         "config": {**workload(cfg, B, k), "parallelism": f"store row-sharded x{world}",
                    "l2": "flushed between steps" if flush else "not flushed",
                    "scan_kernel": kern},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic,
+        "roofline": ({"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                      "frac": achieved / hbm_peak, "traffic": traffic,
+                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"}
+                     if not tensor_bound else
+                     {"bound": "tensor", "achieved": flops / (per_launch_ms / 1e3) / 1e12, "peak": tc_peak,
+                      "unit": "TFLOP/s", "frac": flops / (per_launch_ms / 1e3) / 1e12 / tc_peak,
+                      "traffic": traffic,
+                      "frac_of_sustained": flops / (per_launch_ms / 1e3) / 1e12
+                      / peaks.get("bf16_tflops_sustained", tc_peak),
+                      "hbm_achieved_gbs": achieved,
+                      "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks
+                      else "fallback 2250 (nominal)"}) | {
                      "kernel": kern, "kernel_ms_per_launch": per_launch_ms,
-                     "algorithmic_bytes_per_launch": alg,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
+                     "algorithmic_bytes_per_launch": alg, "algorithmic_flops_per_launch": flops,
                      "kernel_share_of_step": scan_ms_max / max(total_ms, 1e-9)},
         "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": B * cfg.dim * 2,
                 "d2h_bytes_per_step": B * k * 12 + B * cfg.layers * cfg.experts * 4},

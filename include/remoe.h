@@ -230,15 +230,19 @@ REMOE_API remoe_status_t remoe_sps_sync(remoe_sps_t h);
 typedef struct {
   int64_t n_total, n_local, global_offset;
   int32_t dim, n_layers, n_experts, rank, world;
-  int32_t last_scan_kernel;   /* 0 none, 1 streaming (CUDA cores), 2 tensor core (tcgen05) */
+  int32_t last_scan_kernel;   /* 0 none, 1 streaming (CUDA cores), 2 tensor core (tcgen05, resident
+                                 query slab), 3 tensor core on CTA pairs (tcgen05 cta_group::2) */
   int32_t last_launches;      /* kernels launched by the last query (all chunks) */
   int32_t scan_ctas;          /* grid of the scan kernel */
   int64_t device_bytes;       /* store + table + workspaces */
 } remoe_sps_info_t;
 REMOE_API remoe_status_t remoe_sps_get_info(remoe_sps_t h, remoe_sps_info_t* info);
 
-/* Force the scan kernel: 0 auto (default), 1 streaming, 2 tensor core.
- * Also settable with the environment variable REMOE_FORCE_KERNEL=stream|tc. */
+/* Force the scan kernel: 0 auto (default), 1 streaming, 2 tensor core (resident query slab),
+ * 3 tensor core on CTA pairs (the large-batch GEMM tiling).  Auto picks 3 for batches of
+ * at least 256 queries (REMOE_PAIR_MIN_B overrides), else 2 when the store allows it.
+ * Also settable with the environment variable REMOE_FORCE_KERNEL=stream|tc|pair.
+ * INVALID_ARG for other values, UNSUPPORTED when the kernel cannot serve this store. */
 REMOE_API remoe_status_t remoe_sps_set_kernel(remoe_sps_t h, int32_t which);
 
 /*

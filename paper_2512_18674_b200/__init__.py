@@ -4,7 +4,7 @@ The product is libremoe.so (include/remoe.h, CUDA for sm_100a); this package is
 its thin Python binding.  See DESIGN.md.
 """
 from .sps import (  # noqa: F401
-    ABI_FUNCTIONS, KERNEL_AUTO, KERNEL_STREAM, KERNEL_TC, LIB_PATH, RemoeError, Sps, SpsConfig,
+    ABI_FUNCTIONS, KERNEL_AUTO, KERNEL_STREAM, KERNEL_TC, KERNEL_PAIR, LIB_PATH, RemoeError, Sps, SpsConfig,
     SpsInfo, lib, remoe_expert_plan, remoe_nccl_unique_id, remoe_sps_build,
     remoe_sps_config_default, remoe_sps_destroy, remoe_sps_get_info, remoe_sps_profile, remoe_sps_query,
     remoe_sps_query_host, remoe_sps_set_kernel, remoe_sps_sync, remoe_sps_embed, embed, remoe_js_divergence, js_divergence,

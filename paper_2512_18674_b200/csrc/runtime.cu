@@ -123,6 +123,7 @@ struct remoe_sps {
   bool has_tree = false;
   int force_kernel = 0;
   int last_kernel = 0;
+  int pair_min_b = remoe::kPairMinB;  // auto: batches >= this use the CTA-pair scan
   int last_launches = 0;
   size_t device_bytes = 0;
   std::vector<void*> allocs;
@@ -329,6 +330,7 @@ static remoe_status_t build_impl(remoe_sps* h, const uint16_t* emb, const float*
     if (!h->tc_seed.ok) h->seed_rows = 0;
   }
   if (const char* e = getenv("REMOE_SEED")) h->seed_enabled = atoi(e) != 0;
+  if (const char* e = getenv("REMOE_PAIR_MIN_B")) h->pair_min_b = atoi(e);
   ST_TRY(h->alloc((void**)&h->cand_buf, cand_lanes * capmax * 8));
   ST_TRY(h->alloc((void**)&h->lists, (size_t)mb * lists_max * c.max_k * 8));
   ST_TRY(h->alloc((void**)&h->local_top, (size_t)mb * c.max_k * 8));
@@ -346,6 +348,7 @@ static remoe_status_t build_impl(remoe_sps* h, const uint16_t* emb, const float*
   if (const char* f = getenv("REMOE_FORCE_KERNEL")) {
     if (!strcmp(f, "stream")) h->force_kernel = 1;
     else if (!strcmp(f, "tc")) h->force_kernel = 2;
+    else if (!strcmp(f, "pair")) h->force_kernel = 3;
   }
   return REMOE_OK;
 }
@@ -416,8 +419,13 @@ static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k
   ++*launches;
   // ---- S2+S3
   int which = h->force_kernel;
-  if (which == 0) which = (bc <= remoe::kSimtMaxB || !h->tc.ok) ? 1 : 2;
-  if (which == 2 && !h->tc.ok) return fail(REMOE_ERR_UNSUPPORTED, "tensor-core scan unavailable: %s", h->tc.why);
+  if (which == 0) {
+    which = (bc <= remoe::kSimtMaxB || !h->tc.ok) ? 1 : 2;
+    if (which == 2 && bc >= h->pair_min_b && remoe::tc_pair_usable(&h->tc)) which = 3;
+  }
+  if (which >= 2 && !h->tc.ok) return fail(REMOE_ERR_UNSUPPORTED, "tensor-core scan unavailable: %s", h->tc.why);
+  if (which == 3 && !remoe::tc_pair_usable(&h->tc))
+    return fail(REMOE_ERR_UNSUPPORTED, "CTA-pair tensor-core scan unavailable for this store");
   int grid = 0;  // sorted key lists per query produced by the scan
   CUDA_TRY(h->prof_mark(st, true));
   if (which == 1) {
@@ -447,9 +455,11 @@ static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k
       CUDA_TRY(remoe::launch_merge(h->lists, bc, sl, (int64_t)sl * k, k, k, h->seed_top, st, h->gthr));
       ++nl;
     }
-    const remoe_status_t ts = remoe::tc_scan(&h->tc, q, h->qnorm, bc, k, c.sigma, h->xnorm, c.n_local,
-                                             c.global_offset, nullptr, h->cand_buf, h->gthr, h->lists, st,
-                                             &nl, &grid);
+    const remoe_status_t ts =
+        which == 3 ? remoe::tc_pair_scan(&h->tc, q, h->qnorm, bc, k, c.sigma, h->xnorm, c.n_local, c.global_offset,
+                                         nullptr, h->cand_buf, h->gthr, h->lists, st, &nl, &grid)
+                   : remoe::tc_scan(&h->tc, q, h->qnorm, bc, k, c.sigma, h->xnorm, c.n_local, c.global_offset,
+                                    nullptr, h->cand_buf, h->gthr, h->lists, st, &nl, &grid);
     if (ts != REMOE_OK)
       return fail(ts, "tensor-core scan launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     *launches += nl;
@@ -669,15 +679,17 @@ remoe_status_t remoe_sps_get_info(remoe_sps_t h, remoe_sps_info_t* info) {
   info->world = h->cfg.world;
   info->last_scan_kernel = h->last_kernel;
   info->last_launches = h->last_launches;
-  info->scan_ctas = h->last_kernel == 2 ? h->grid_tc : h->grid_simt;
+  info->scan_ctas = h->last_kernel >= 2 ? h->grid_tc : h->grid_simt;
   info->device_bytes = (int64_t)h->device_bytes;
   return REMOE_OK;
 }
 
 remoe_status_t remoe_sps_set_kernel(remoe_sps_t h, int32_t which) {
   if (!h) return fail(REMOE_ERR_STATE, "handle is NULL");
-  if (which < 0 || which > 2) return fail(REMOE_ERR_INVALID_ARG, "which must be 0, 1 or 2");
-  if (which == 2 && !h->tc.ok) return fail(REMOE_ERR_UNSUPPORTED, "tensor-core scan unavailable: %s", h->tc.why);
+  if (which < 0 || which > 3) return fail(REMOE_ERR_INVALID_ARG, "which must be 0, 1, 2 or 3");
+  if (which >= 2 && !h->tc.ok) return fail(REMOE_ERR_UNSUPPORTED, "tensor-core scan unavailable: %s", h->tc.why);
+  if (which == 3 && !remoe::tc_pair_usable(&h->tc))
+    return fail(REMOE_ERR_UNSUPPORTED, "CTA-pair tensor-core scan unavailable for this store");
   h->force_kernel = which;
   return REMOE_OK;
 }

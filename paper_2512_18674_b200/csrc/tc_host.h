@@ -32,6 +32,16 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
                        const float* xnorm, int64_t n_rows, int64_t gid_offset, const int64_t* gid_map,
                        uint64_t* cand_buf, unsigned long long* gthr, uint64_t* lists, cudaStream_t st,
                        int* launches, int* lists_per_query);
+// Large batches: the CTA-pair (cta_group::2) GEMM-tiled scan (k_scan_pair.cu), same
+// output contract as tc_scan; 256 queries per pair.
+bool tc_pair_usable(const TcPlan* t);
+remoe_status_t tc_pair_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc, int k, float sigma,
+                            const float* xnorm, int64_t n_rows, int64_t gid_offset, const int64_t* gid_map,
+                            uint64_t* cand_buf, unsigned long long* gthr, uint64_t* lists, cudaStream_t st,
+                            int* launches, int* lists_per_query);
+// Batches of at least this many queries use the pair scan (REMOE_PAIR_MIN_B overrides).
+constexpr int kPairMinB = 256;
+
 // Largest lists_per_query tc_scan can produce (workspace sizing).
 constexpr int kTcMaxStatesPerCta = 2;
 constexpr int kTcEpilogueThreads = 256;

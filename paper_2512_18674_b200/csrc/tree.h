@@ -12,7 +12,7 @@
 namespace remoe {
 
 constexpr int kTreeCMax = 16;      // branching limit (register accumulators in k_assign)
-constexpr int kTreeMaxDepth = 64;  // path storage in the search kernel
+constexpr int kTreeMaxDepth = 128;  // path storage in the search kernel (the synthetic stores reach ~70 levels: noise outliers peel off one at a time)
 constexpr int kTreeCandCap = 2048; // candidate keys per query in shared memory
 
 // Flat tree, breadth-first node numbering (root 0).  Node i owns perm[begin[i], end[i]);

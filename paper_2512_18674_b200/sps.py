@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libremoe.so")
 
 REMOE_OK = 0
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "CUDA", 3: "NCCL", 4: "OOM", 5: "UNSUPPORTED", 6: "STATE"}
-KERNEL_AUTO, KERNEL_STREAM, KERNEL_TC = 0, 1, 2
+KERNEL_AUTO, KERNEL_STREAM, KERNEL_TC, KERNEL_PAIR = 0, 1, 2, 3
 
 # every function declared in include/remoe.h
 ABI_FUNCTIONS = (

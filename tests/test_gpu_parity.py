@@ -19,7 +19,7 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU box
 
 import paper_2512_18674_b200 as remoe  # noqa: E402
 
-KERNELS = {"stream": remoe.KERNEL_STREAM, "tc": remoe.KERNEL_TC}
+KERNELS = {"stream": remoe.KERNEL_STREAM, "tc": remoe.KERNEL_TC, "pair": remoe.KERNEL_PAIR}
 
 
 def _store(name, n=None):
@@ -65,7 +65,7 @@ def assert_parity(rep):
 
 # ------------------------------------------------------------------ tiny: everything, full
 
-@pytest.mark.parametrize("kern", ["stream", "tc"])
+@pytest.mark.parametrize("kern", ["stream", "tc", "pair"])
 def test_tiny_full(kern):
     c, x, a = store("tiny")
     q = gen.queries(c.store_seed, c.query_seed, c.n, c.dim, c.batch, mode=1)
@@ -99,7 +99,7 @@ def c2_oracle(B, k):
     return _C2Q[key]
 
 
-@pytest.mark.parametrize("kern", ["stream", "tc"])
+@pytest.mark.parametrize("kern", ["stream", "tc", "pair"])
 @pytest.mark.parametrize("B", [1, 2, 3, 4, 8, 16, 64, 256])
 def test_c2_batch_sweep(kern, B):
     c, x, a = store("c2")
@@ -117,7 +117,7 @@ def test_c2_batch_sweep(kern, B):
     assert rep.substitutions == 0, "c2 is well separated at k=10: ids must match exactly"
 
 
-@pytest.mark.parametrize("kern", ["stream", "tc"])
+@pytest.mark.parametrize("kern", ["stream", "tc", "pair"])
 @pytest.mark.parametrize("k", [1, 2, 5, 16, 32, 64, 128, 256])
 def test_c2_k_sweep(kern, k):
     c, x, a = store("c2", 20_000)
@@ -132,7 +132,7 @@ def test_c2_k_sweep(kern, k):
 
 # ------------------------------------------------------------------ invariants
 
-@pytest.mark.parametrize("kern", ["stream", "tc"])
+@pytest.mark.parametrize("kern", ["stream", "tc", "pair"])
 def test_invariants_rerun_batch_order_k1(kern):
     c, x, a = store("c2", 30_000)
     q = gen.queries(c.store_seed, c.query_seed, 30_000, c.dim, 24, mode=1)
@@ -164,7 +164,7 @@ def test_invariants_rerun_batch_order_k1(kern):
 
 # ------------------------------------------------------------------ edge cases
 
-@pytest.mark.parametrize("kern", ["stream", "tc"])
+@pytest.mark.parametrize("kern", ["stream", "tc", "pair"])
 @pytest.mark.parametrize("n", [1, 2, 7, 64, 149, 300])
 def test_small_stores_k_equals_n(kern, n):
     """Fewer rows than CTAs, k = N returns every row in key order."""
@@ -181,7 +181,7 @@ def test_small_stores_k_equals_n(kern, n):
         assert sorted(ids[i].tolist()) == sorted(set(ids[i].tolist()))
 
 
-@pytest.mark.parametrize("kern", ["stream", "tc"])
+@pytest.mark.parametrize("kern", ["stream", "tc", "pair"])
 def test_degenerate_rows(kern):
     """Zero rows score 0; exact duplicate rows tie and the lower id comes first;
     a zero query scores 0 everywhere (sigma keeps it finite)."""
@@ -210,7 +210,7 @@ def test_dims_and_table_shapes():
         a /= a.sum(-1, keepdims=True)
         q = gen.f32_to_bf16_bits(rng.standard_normal((6, D)).astype(np.float32))
         s = make(x, a, max_k=32)
-        for kern in ("stream", "tc"):
+        for kern in ("stream", "tc", "pair"):
             if not kernel_available(s, kern):
                 continue
             ids, sc, pred = run(s, q, 9)
@@ -281,7 +281,7 @@ def test_expert_plan_vs_oracle():
 
 # ------------------------------------------------------------------ full-size sampled parity
 
-@pytest.mark.parametrize("kern", ["stream", "tc"])
+@pytest.mark.parametrize("kern", ["stream", "tc", "pair"])
 def test_c3_full_size_sampled(kern):
     """BASELINE c3 (1M x 1024, 24x60, k=16) at its bench batch B=64 (and B=4 for the
     streaming kernel); 6 sampled queries checked against the oracle one by one."""
