@@ -73,7 +73,7 @@ __device__ __forceinline__ void block_sort_desc(uint64_t* a, int np2) {
 }
 
 __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, int n_lists,
-                                               int64_t qstride, int64_t lstride, int k,
+                                               int64_t qstride, int64_t lstride, int list_len, int k,
                                                uint64_t* __restrict__ out,
                                                unsigned long long* __restrict__ set_thr,
                                                const unsigned long long* __restrict__ lower,
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
   const int b = blockIdx.x;
   pdl_wait();  // the scan's lists and thresholds
   const uint64_t* base = in + (int64_t)b * qstride;
-  const int nch = (k + 31) >> 5;
+  const int nch = (list_len + 31) >> 5;
   const int items = n_lists * nch;
   uint64_t lb = lower ? lower[b] : 0ull;
   if (lb == 0) lb = 1;  // sentinel keys (0) never count
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
     if (it >= items) return 0ull;
     const int l = nch == 1 ? it : it / nch, c = it - l * nch;
     const int i = c * 32 + lane;
-    return i < k ? __ldg(base + (int64_t)l * lstride + i) : 0ull;
+    return i < list_len ? __ldg(base + (int64_t)l * lstride + i) : 0ull;
   };
   auto collect = [&](uint64_t thr_lo) {  // append keys >= thr_lo to cand (warp-aggregated)
     for (int it0 = warp; it0 < items; it0 += 8 * 4) {
@@ -220,14 +220,15 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
 
 cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride, int64_t lstride,
                          int k, uint64_t* out, cudaStream_t st, unsigned long long* set_thr,
-                         const unsigned long long* lower, const FinalizeArgs* fin) {
+                         const unsigned long long* lower, const FinalizeArgs* fin, int list_len) {
   if (B <= 0) return cudaSuccess;
   if (k > 256) return cudaErrorInvalidValue;
+  if (list_len <= 0) list_len = k;
   FinalizeArgs f{};
   if (fin) f = *fin;
   cudaError_t e = set_smem_attrs_once((const void*)k_merge, 0);
   if (e != cudaSuccess) return e;
-  return launch_pdl(k_merge, dim3(B), dim3(256), 0, st, in, n_lists, qstride, lstride, k, out, set_thr,
+  return launch_pdl(k_merge, dim3(B), dim3(256), 0, st, in, n_lists, qstride, lstride, list_len, k, out, set_thr,
                     lower, f);
 }
 

@@ -439,16 +439,18 @@ remoe_status_t tc_pair_scan(TcPlan* t, const uint16_t* q, const float* qnorm, in
   const bool in_cta = k <= 32 && (size_t)nst * kBox >= (size_t)kTcEpilogueThreads * KR * 8;
   const int lists_per_cta = in_cta ? 1 : 2;
   // Query groups of 256 (one per pair); every group's pairs walk the store tiles in the
-  // same order, so a tile is read from HBM once and by the other groups from L2.  Groups
-  // per launch: the count that keeps the most pairs busy over all launches.
+  // same order, so a tile is read from HBM once per launch and by the other groups from
+  // L2.  Groups per launch g: minimise launches x (one store read + the launch's MMA time
+  // on g * floor(pairs / g) pairs), with one group's MMA time ~ one store read (the ridge,
+  // B ~ 254, is about one group of 256); overlap is not assumed.
   const int pairs_max = t->grid / 2;
   const int n_groups = (bc + 2 * kQPerCta - 1) / (2 * kQPerCta);
   int best_g = 1;
-  double best_eff = 0;
+  double best_cost = 1e300;
   for (int g = 1; g <= (n_groups < pairs_max ? n_groups : pairs_max); ++g) {
     const int nl = (n_groups + g - 1) / g;
-    const double eff = (double)n_groups / ((double)nl * g) * (double)(g * (pairs_max / g)) / pairs_max;
-    if (eff > best_eff + 1e-9) { best_eff = eff; best_g = g; }
+    const double cost = nl * (1.0 + (double)g * pairs_max / (double)(g * (pairs_max / g)));
+    if (cost < best_cost - 1e-9) { best_cost = cost; best_g = g; }
   }
   const int gpl = best_g;
   const int ppg = pairs_max / gpl;  // pairs per group

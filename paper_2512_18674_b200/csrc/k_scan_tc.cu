@@ -436,7 +436,8 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   CUtensorMapFloatOOBfill);
 
 remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int dim, int num_sms,
-                              int max_k) {
+                              int max_k, int64_t row_stride) {
+  if (row_stride <= 0) row_stride = dim;
   (void)max_k;
   t->ok = false;
   t->x = x;
@@ -455,7 +456,7 @@ remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int 
     return REMOE_OK;
   }
   const cuuint64_t gdim[2] = {(cuuint64_t)dim, (cuuint64_t)n_rows};
-  const cuuint64_t gstride[1] = {(cuuint64_t)dim * 2};
+  const cuuint64_t gstride[1] = {(cuuint64_t)row_stride * 2};
   const cuuint32_t box[2] = {(cuuint32_t)kBlockK, (cuuint32_t)kTileN};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = ((EncodeTiledFn)fn)(reinterpret_cast<CUtensorMap*>(t->tmap_x), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,

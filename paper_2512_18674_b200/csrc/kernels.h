@@ -49,14 +49,16 @@ struct FinalizeArgs {
   float* pred;  // may be null: ids and scores only
 };
 
-// S4 / S5: per query, merge n_lists sorted key lists of length k into the best k.
+// S4 / S5: per query, merge n_lists sorted key lists of length list_len (default k) into
+// the best k.
 // key(b, l, i) = in[b * qstride + l * lstride + i].  Keys below lower[b] (a known lower
 // bound of the final k-th best key) are dropped.  If set_thr is non-null, also
 // set_thr[b] = (k-th best key) - 1 (threshold seeding from a row sample).  If fin is
 // non-null the same CTA then runs S6 + S7 for the query (fused finalize).
 cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride, int64_t lstride,
                          int k, uint64_t* out, cudaStream_t st, unsigned long long* set_thr = nullptr,
-                         const unsigned long long* lower = nullptr, const FinalizeArgs* fin = nullptr);
+                         const unsigned long long* lower = nullptr, const FinalizeArgs* fin = nullptr,
+                         int list_len = -1);
 
 // S6 + S7 as a separate kernel (multi-GPU path, after the row exchange).
 cudaError_t launch_finalize(const uint64_t* top, int B, int k, const float* act, int64_t offset,

@@ -112,11 +112,13 @@ struct remoe_sps {
   // k-th best key - 1 is a strict lower bound that the full scan starts from
   remoe::TcPlan tc_seed{};
   int64_t seed_rows = 0;
-  uint16_t* xs = nullptr;
   float* xns = nullptr;
   int64_t* gids = nullptr;
   uint64_t* seed_top = nullptr;
-  bool seed_enabled = false;  // REMOE_SEED=1: measured net-negative at small B so far
+  // -1 auto: seed when k > 32 (the buffer top-k, whose warm-up inserts dominate without a
+  // threshold); 1 always (REMOE_SEED=1); 0 never (REMOE_SEED=0).  For k <= 32 the register
+  // top-k settles within a tile and seeding was measured net-negative.
+  int seed_mode = -1;
   ncclComm_t comm = nullptr;
   // NEXT-N2 clustering tree over this shard (remoe_sps_tree_build)
   remoe::Tree tree{};
@@ -310,26 +312,25 @@ static remoe_status_t build_impl(remoe_sps* h, const uint16_t* emb, const float*
   const int mb = c.max_batch;
   ST_TRY(h->alloc((void**)&h->qnorm, (size_t)mb * 4));
   ST_TRY(h->alloc((void**)&h->gthr, (size_t)2 * mb * 8));  // [0, mb): main scan, [mb, 2mb): seed scan
-  // ---- seeding sample: S rows j * stride, S a multiple of 128, only for large shards
+  // ---- seeding sample: S rows j * stride, S a multiple
+  // of 128, only for large shards.  The sample is read in place through a strided tensor
+  // map; only its norms and global ids are copied.
   if (h->tc.ok && c.n_local >= 32 * 2048) {
-    const int64_t S = 2048;
-    const int64_t stride = c.n_local / S;
+    const int64_t stride = std::min<int64_t>(16, c.n_local / 2048);
+    const int64_t S = (c.n_local / stride) / 128 * 128;
     h->seed_rows = S;
-    ST_TRY(h->alloc((void**)&h->xs, (size_t)S * c.dim * 2));
     ST_TRY(h->alloc((void**)&h->xns, (size_t)S * 4));
     ST_TRY(h->alloc((void**)&h->gids, (size_t)S * 8));
     ST_TRY(h->alloc((void**)&h->seed_top, (size_t)mb * c.max_k * 8));
-    CUDA_TRY(cudaMemcpy2DAsync(h->xs, (size_t)c.dim * 2, h->x, (size_t)stride * c.dim * 2, (size_t)c.dim * 2, S,
-                               cudaMemcpyDeviceToDevice, st));
     CUDA_TRY(cudaMemcpy2DAsync(h->xns, 4, h->xnorm, (size_t)stride * 4, 4, S, cudaMemcpyDeviceToDevice, st));
     std::vector<int64_t> g(S);
     for (int64_t j = 0; j < S; ++j) g[j] = c.global_offset + j * stride;
     CUDA_TRY(cudaMemcpyAsync(h->gids, g.data(), S * 8, cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    ST_TRY(remoe::tc_plan_create(&h->tc_seed, h->xs, S, c.dim, h->num_sms, c.max_k));
+    ST_TRY(remoe::tc_plan_create(&h->tc_seed, h->x, S, c.dim, h->num_sms, c.max_k, stride * c.dim));
     if (!h->tc_seed.ok) h->seed_rows = 0;
   }
-  if (const char* e = getenv("REMOE_SEED")) h->seed_enabled = atoi(e) != 0;
+  if (const char* e = getenv("REMOE_SEED")) h->seed_mode = atoi(e) != 0 ? 1 : 0;
   if (const char* e = getenv("REMOE_PAIR_MIN_B")) h->pair_min_b = atoi(e);
   ST_TRY(h->alloc((void**)&h->cand_buf, cand_lanes * capmax * 8));
   ST_TRY(h->alloc((void**)&h->lists, (size_t)mb * lists_max * c.max_k * 8));
@@ -445,14 +446,23 @@ static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k
     }
   } else {
     int nl = 0;
-    if (h->seed_rows > 0 && h->seed_enabled && 8 * k <= h->seed_rows) {
+    const bool seed = h->seed_mode == 1 || (h->seed_mode == -1 && k > 32);
+    if (h->seed_rows > 0 && seed && 8 * k <= h->seed_rows) {
+      // Scan the sample with the register top-k (k_s = min(k, 32) per state): the k-th best
+      // key of the union of the per-state lists is a real key of the store, hence a lower
+      // bound of the final k-th best; minus one it seeds the thresholds (strict bound).
+      const int ks = std::min(k, 32);
       int sl = 0;
-      const remoe_status_t ss = remoe::tc_scan(&h->tc_seed, q, h->qnorm, bc, k, c.sigma, h->xns, h->seed_rows,
-                                               0, h->gids, h->cand_buf, h->gthr + c.max_batch, h->lists, st,
-                                               &nl, &sl);
+      const remoe_status_t ss =
+          which == 3 ? remoe::tc_pair_scan(&h->tc_seed, q, h->qnorm, bc, ks, c.sigma, h->xns, h->seed_rows, 0,
+                                           h->gids, h->cand_buf, h->gthr + c.max_batch, h->lists, st, &nl, &sl)
+                     : remoe::tc_scan(&h->tc_seed, q, h->qnorm, bc, ks, c.sigma, h->xns, h->seed_rows, 0, h->gids,
+                                      h->cand_buf, h->gthr + c.max_batch, h->lists, st, &nl, &sl);
       if (ss != REMOE_OK)
         return fail(ss, "seed scan launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-      CUDA_TRY(remoe::launch_merge(h->lists, bc, sl, (int64_t)sl * k, k, k, h->seed_top, st, h->gthr));
+      if ((int64_t)sl * ks < k) return fail(REMOE_ERR_STATE, "seed sample too small for k=%d", k);
+      CUDA_TRY(remoe::launch_merge(h->lists, bc, sl, (int64_t)sl * ks, ks, k, h->seed_top, st, h->gthr, nullptr,
+                                   nullptr, ks));
       ++nl;
     }
     const remoe_status_t ts =

@@ -21,8 +21,10 @@ struct TcPlan {
   int dim = 0;
 };
 
+// row_stride: elements between consecutive rows (default dim; a multiple of dim selects
+// every (row_stride/dim)-th row of the store, e.g. the threshold-seeding sample).
 remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int dim, int num_sms,
-                              int max_k);
+                              int max_k, int64_t row_stride = 0);
 void tc_plan_destroy(TcPlan* t);
 // Scores bc queries (any bc >= 1; 64 or 128 queries per pass) and writes sorted
 // top-k key lists: *lists_per_query lists of k keys per query,
@@ -40,7 +42,7 @@ remoe_status_t tc_pair_scan(TcPlan* t, const uint16_t* q, const float* qnorm, in
                             uint64_t* cand_buf, unsigned long long* gthr, uint64_t* lists, cudaStream_t st,
                             int* launches, int* lists_per_query);
 // Batches of at least this many queries use the pair scan (REMOE_PAIR_MIN_B overrides).
-constexpr int kPairMinB = 256;
+constexpr int kPairMinB = 128;
 
 // Largest lists_per_query tc_scan can produce (workspace sizing).
 constexpr int kTcMaxStatesPerCta = 2;

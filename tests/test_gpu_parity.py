@@ -327,3 +327,21 @@ def test_c5_sweep_corners_sampled(k):
     # identical queries (i % 8 == 7 duplicates i - 1) across chunk boundaries
     for i in (7, 1031, 4095):
         assert np.array_equal(ids[i], ids[i - 1]) and np.array_equal(pred[i], pred[i - 1])
+
+
+@pytest.mark.parametrize("kern", ["tc", "pair"])
+@pytest.mark.parametrize("k", [33, 64, 128, 256])
+def test_seeded_large_k(kern, k):
+    """k > 32 seeds the shared thresholds from a strided sample (every 16th row, scanned
+    with the register top-32 per state): results must
+    still equal the oracle's exactly, including when the sample holds the winners."""
+    c, x, a = store("c2", 200_000)
+    q = gen.queries(c.store_seed, c.query_seed, 200_000, c.dim, 40, mode=1)
+    q[3] = x[16 * 7]          # an exact copy of a sampled row
+    q[4] = x[16 * 7 + 1]      # ... and of an unsampled neighbour
+    s = make(x, a, max_k=256)
+    if not kernel_available(s, kern):
+        pytest.skip(f"{kern} kernel unavailable")
+    ids, sc, pred = run(s, q, k)
+    assert_parity(compare(q, x, a, k, ids, sc, pred))
+    assert ids[3, 0] == 16 * 7 and ids[4, 0] == 16 * 7 + 1
