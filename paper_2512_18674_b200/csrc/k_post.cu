@@ -98,13 +98,21 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
     const int i = c * 32 + lane;
     return i < list_len ? __ldg(base + (int64_t)l * lstride + i) : 0ull;
   };
+  // flat key f = l * list_len + i: the whole block reads 8 keys per thread per round
+  // (one L2 round trip per 2048 keys, instead of one per 32 lists of a warp)
+  const int64_t n_keys = (int64_t)n_lists * list_len;
+  auto flat_key = [&](int64_t f) -> uint64_t {
+    if (f >= n_keys) return 0ull;
+    const int64_t l = f / list_len, i = f - l * list_len;
+    return __ldg(base + l * lstride + i);
+  };
   auto collect = [&](uint64_t thr_lo) {  // append keys >= thr_lo to cand (warp-aggregated)
-    for (int it0 = warp; it0 < items; it0 += 8 * 4) {
-      uint64_t kk[4];
+    for (int64_t f0 = (int64_t)warp * 32 + lane; f0 - lane < n_keys; f0 += 8 * 256) {
+      uint64_t kk[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) kk[u] = item_key(it0 + 8 * u);
+      for (int u = 0; u < 8; ++u) kk[u] = flat_key(f0 + 256 * u);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 8; ++u) {
         const unsigned m = __ballot_sync(kFull, kk[u] >= thr_lo);
         if (m) {
           int pos0 = 0;
@@ -275,6 +283,39 @@ __device__ __forceinline__ void finalize_query(const uint64_t* tb, int k, int b,
   for (int i = 0; i < 8; ++i) Z += red[i];
   if (t < k) w[t] = __fdiv_rn(e, Z);
   __syncthreads();
+  if ((f.LE & 3) == 0 && (j0 & 3) == 0 && ((j1 & 3) == 0 || j1 == f.LE)) {
+    // float4 columns, two per thread per step, 8 rows at a time (16 x 16-byte loads in
+    // flight): per element the same r-ascending FMA chain as the scalar path below
+    const int64_t c0 = j0 >> 2, c1 = (j1 + 3) >> 2;
+    for (int64_t ca = c0 + t; ca < c1; ca += 2 * (int64_t)blockDim.x) {
+      const int64_t cb = ca + blockDim.x;
+      const bool vb = cb < c1;
+      float4 acc_a = make_float4(0.f, 0.f, 0.f, 0.f), acc_b = acc_a;
+      for (int r0 = 0; r0 < k; r0 += 8) {
+        float4 xa[8], xb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const bool vr = r0 + u < k;
+          const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+          xa[u] = vr ? __ldg(reinterpret_cast<const float4*>(src[r0 + u]) + ca) : z;
+          xb[u] = (vr && vb) ? __ldg(reinterpret_cast<const float4*>(src[r0 + u]) + cb) : z;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (r0 + u < k) {  // r ascending
+            const float wr = w[r0 + u];
+            acc_a.x = __fmaf_rn(wr, xa[u].x, acc_a.x); acc_a.y = __fmaf_rn(wr, xa[u].y, acc_a.y);
+            acc_a.z = __fmaf_rn(wr, xa[u].z, acc_a.z); acc_a.w = __fmaf_rn(wr, xa[u].w, acc_a.w);
+            acc_b.x = __fmaf_rn(wr, xb[u].x, acc_b.x); acc_b.y = __fmaf_rn(wr, xb[u].y, acc_b.y);
+            acc_b.z = __fmaf_rn(wr, xb[u].z, acc_b.z); acc_b.w = __fmaf_rn(wr, xb[u].w, acc_b.w);
+          }
+        }
+      }
+      reinterpret_cast<float4*>(f.pred + (int64_t)b * f.LE)[ca] = acc_a;
+      if (vb) reinterpret_cast<float4*>(f.pred + (int64_t)b * f.LE)[cb] = acc_b;
+    }
+    return;
+  }
   // two outputs per thread per step, 8 rows at a time: 16 independent loads in flight
   for (int64_t ja = j0 + t; ja < j1; ja += 2 * (int64_t)blockDim.x) {
     const int64_t jb = ja + blockDim.x;

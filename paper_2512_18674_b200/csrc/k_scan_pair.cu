@@ -68,6 +68,7 @@ struct PairArgs {
   uint64_t* out;           // lists[(q * lists_per_query + l) * k + i]
   int smem_bufs;
   int merge_in_cta;
+  int kb_order;            // K-block visiting order (kb_at)
 };
 }  // namespace
 
@@ -128,7 +129,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
       int it = 0;
       for (int64_t t = pair; t < n_tiles; t += npairs) {
         const int xrow = (int)(t * kPairN) + (int)crank * 128;
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
+        for (int j = 0; j < nkb; ++j, ++it) {
+          const int kb = kb_at(j, nkb, p.kb_order);
           const int s = it % NST;
           const uint32_t ph = (uint32_t)(it / NST) & 1u;
           mbar_wait(&empty[s], ph ^ 1u);  // the pair's MMA is done with this CTA's slot
@@ -153,7 +155,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         mbar_wait(&tempty[acc], aph ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kPairN);
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
+        for (int j = 0; j < nkb; ++j, ++it) {
           const int s = it % NST;
           const uint32_t ph = (uint32_t)(it / NST) & 1u;
           mbar_wait(&full[s], ph);
@@ -163,7 +165,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < kPBK / 16; ++kk)
             umma_bf16_pair(d_tmem, umma_desc(abase + kk * 32), umma_desc(bbase + kk * 32), idesc,
-                           (kb | kk) != 0);
+                           (j | kk) != 0);
           umma_commit_pair(&empty[s], 3);  // frees slot s in both CTAs
         }
         umma_commit_pair(&tfull[acc], 3);  // accumulator ready in both CTAs
@@ -466,10 +468,11 @@ remoe_status_t tc_pair_scan(TcPlan* t, const uint16_t* q, const float* qnorm, in
     const cuuint32_t box[2] = {(cuuint32_t)kPBK, 128u};
     const cuuint32_t estr[2] = {1, 1};
     if (enc(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(q + (size_t)s0 * D), gdim, gstride,
-            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, tmap_promotion(),
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return REMOE_ERR_CUDA;
     PairArgs a{};
+    a.kb_order = kb_order_env();
     a.xnorm = xnorm;
     a.n_rows = n_rows;
     a.gid_offset = gid_offset;

@@ -63,6 +63,8 @@ struct TcArgs {
   int merge_in_cta;        // register top-k: merge the two parity states into one list per CTA
   int cluster;             // CTAs per cluster along y (multicast of the store tiles), 1 = none
   int epi_sleep;           // epilogue waits with a suspend-time hint (REMOE_EPI_SLEEP=1)
+  const uint16_t* xt;      // tiled store (TcPlan::xt): 1-D bulk copies, else the tensor map
+  int kb_order;            // K-block visiting order (kb_at)
   unsigned long long* stats;  // REMOE_TC_STATS: [0] candidate columns, [1] inserts, [2] chunks with a candidate
 };
 }  // namespace
@@ -166,17 +168,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int it = 0;
       for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
+        for (int j = 0; j < nkb; ++j, ++it) {
+          const int kb = kb_at(j, nkb, p.kb_order);
           const int s = it % NST;
           const uint32_t ph = (uint32_t)(it / NST) & 1u;
           mbar_wait(&empty[s], ph ^ 1u);  // this CTA's MMA is done with the slot
           mbar_arrive_expect_tx(&full[s], kStageBytes);
+          // tiled store: box (t, kb) is 16 KB contiguous in HBM, already in the swizzled
+          // UMMA layout, so a 1-D bulk copy streams it (no 128 B-per-row DRAM pattern)
+          const uint16_t* src = p.xt ? p.xt + ((size_t)t * nkb + kb) * (kStageBytes / 2) : nullptr;
           if (C == 1) {
-            tma_load_2d(sB + (size_t)s * kStageBytes, &tmap_x, kb * kBlockK, (int)(t * kTileN), &full[s]);
+            if (src) bulk_g2s(sB + (size_t)s * kStageBytes, src, kStageBytes, &full[s]);
+            else tma_load_2d(sB + (size_t)s * kStageBytes, &tmap_x, kb * kBlockK, (int)(t * kTileN), &full[s]);
           } else if (crank == 0) {
             mbar_wait(&cempty[s], ph ^ 1u);  // every CTA of the cluster is done with the slot
-            tma_load_2d_mc(sB + (size_t)s * kStageBytes, &tmap_x, kb * kBlockK, (int)(t * kTileN), &full[s],
-                           (uint16_t)((1u << C) - 1u));
+            if (src)
+              bulk_g2s_mc(sB + (size_t)s * kStageBytes, src, kStageBytes, &full[s], (uint16_t)((1u << C) - 1u));
+            else
+              tma_load_2d_mc(sB + (size_t)s * kStageBytes, &tmap_x, kb * kBlockK, (int)(t * kTileN), &full[s],
+                             (uint16_t)((1u << C) - 1u));
           }
         }
       }
@@ -196,7 +206,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty[acc], aph ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kTileN);
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
+        for (int j = 0; j < nkb; ++j, ++it) {
+          const int kb = kb_at(j, nkb, p.kb_order);
           const int s = it % NST;
           const uint32_t ph = (uint32_t)(it / NST) & 1u;
           mbar_wait(&full[s], ph);
@@ -206,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < kBlockK / 16; ++kk)
             umma_bf16(d_tmem, umma_desc(abase + kk * 32), umma_desc(bbase + kk * 32), idesc,
-                      (kb | kk) != 0);
+                      (j | kk) != 0);
           umma_commit(&empty[s]);
           if (C > 1) umma_commit_mc(&cempty[s], 1);  // the leader's slot-free barrier
         }
@@ -417,6 +428,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------------ tiled store
+// xt box (tile, kb) = rows tile*128 .. +127, elements kb*64 .. +63, laid out exactly as
+// the UMMA reads a SWIZZLE_128B K-major operand from a 1024-byte aligned stage: row r at
+// r*128 bytes, its 16-byte chunk c at ((c ^ (r & 7)) * 16).  One thread per 16-byte chunk.
+__global__ void k_tile_store(const uint4* __restrict__ x, int64_t n_rows, int dim, uint4* __restrict__ xt) {
+  const int cpr = dim / 8;  // 16-byte chunks per row
+  const int64_t n_tiles = (n_rows + kTileN - 1) / kTileN;
+  const int64_t total = n_tiles * kTileN * cpr;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / cpr;
+    const int cc = (int)(i - row * cpr);
+    const int kb = cc >> 3, c = cc & 7, r = (int)(row % kTileN);
+    const int64_t tile = row / kTileN;
+    const uint4 v = row < n_rows ? x[i] : make_uint4(0u, 0u, 0u, 0u);
+    xt[((tile * (cpr >> 3) + kb) * kTileN + r) * 8 + (c ^ (r & 7))] = v;
+  }
+}
+
+cudaError_t tc_tile_store(const uint16_t* x, int64_t n_rows, int dim, uint16_t* xt, cudaStream_t st) {
+  if (dim % kBlockK != 0 || n_rows <= 0) return cudaErrorInvalidValue;
+  k_tile_store<<<1184, 256, 0, st>>>(reinterpret_cast<const uint4*>(x), n_rows, dim, reinterpret_cast<uint4*>(xt));
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ host side
 
 static size_t tc_smem(int M, int D, int nst, int buf_bytes) {
@@ -443,6 +478,7 @@ remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int 
   t->x = x;
   t->n_rows = n_rows;
   t->dim = dim;
+  t->row_stride = row_stride;
   t->grid = 0;
   t->threads_per_cta_queries = kTcEpilogueThreads;
   if (dim % kBlockK != 0) { t->why = "D % 64 != 0"; return REMOE_OK; }
@@ -462,7 +498,7 @@ remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int 
   CUresult r = ((EncodeTiledFn)fn)(reinterpret_cast<CUtensorMap*>(t->tmap_x), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                                    const_cast<uint16_t*>(x), gdim, gstride, box, estr,
                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   tmap_promotion(),
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) { t->why = "cuTensorMapEncodeTiled failed"; return REMOE_OK; }
   const int64_t n_tiles = (n_rows + kTileN - 1) / kTileN;
@@ -567,6 +603,8 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
     a.smem_bufs = smem_bufs ? 1 : 0;
     a.cluster = getenv("REMOE_NO_MULTICAST") ? 1 : 8;  // reduced to what fits in launch_tc_t
     a.epi_sleep = getenv("REMOE_EPI_SLEEP") ? atoi(getenv("REMOE_EPI_SLEEP")) : 0;
+    a.xt = t->xt;
+    a.kb_order = kb_order_env();
     static unsigned long long* stats = nullptr;
     if (getenv("REMOE_TC_STATS")) {
       if (!stats) { cudaMalloc(&stats, 3 * 8); }

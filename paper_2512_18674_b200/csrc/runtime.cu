@@ -90,6 +90,7 @@ struct remoe_sps {
   int stage_rows = 0;
   // store
   uint16_t* x = nullptr;
+  uint16_t* xt = nullptr;  // tiled copy for the tensor-core scan (or nullptr)
   float* xnorm = nullptr;
   float* act = nullptr;
   // workspaces
@@ -115,10 +116,13 @@ struct remoe_sps {
   float* xns = nullptr;
   int64_t* gids = nullptr;
   uint64_t* seed_top = nullptr;
-  // -1 auto: seed when k > 32 (the buffer top-k, whose warm-up inserts dominate without a
-  // threshold); 1 always (REMOE_SEED=1); 0 never (REMOE_SEED=0).  For k <= 32 the register
-  // top-k settles within a tile and seeding was measured net-negative.
+  // -1 auto: seed when k > 32 or B >= seed_min_b; 1 always (REMOE_SEED=1); 0 never
+  // (REMOE_SEED=0).  Without a seed every top-k state (a CTA's rows for one query) starts
+  // from nothing and inserts ~k(1 + ln(R/k)) keys, most of them in the first tiles, when
+  // all SMs insert at once and the store stream stalls (ncu PM sampling, profiles/).
   int seed_mode = -1;
+  int seed_min_b = remoe::kSeedMinB;
+  int seed_ks = 0;       // per-state list length of the seed scan (0: seed_ks_for(k))
   ncclComm_t comm = nullptr;
   // NEXT-N2 clustering tree over this shard (remoe_sps_tree_build)
   remoe::Tree tree{};
@@ -306,6 +310,15 @@ static remoe_status_t build_impl(remoe_sps* h, const uint16_t* emb, const float*
   const int capmax = 32 * remoe::topk_P(c.max_k);
   ST_TRY(remoe::tc_plan_create(&h->tc, h->x, c.n_local, c.dim, h->num_sms, c.max_k));
   h->grid_tc = h->tc.grid;
+  // Tiled, pre-swizzled copy of the store for the tensor-core scan: every
+  // 16 KB box the scan loads is one contiguous range of HBM.  REMOE_TC_TILED=0 keeps the
+  // 2-D tensor-map loads of the row-major store (and saves the copy's memory).
+  const char* tiled_env = getenv("REMOE_TC_TILED");
+  if (h->tc.ok && !(tiled_env && atoi(tiled_env) == 0)) {
+    ST_TRY(h->alloc((void**)&h->xt, remoe::tc_tiled_bytes(c.n_local, c.dim)));
+    CUDA_TRY(remoe::tc_tile_store(h->x, c.n_local, c.dim, h->xt, st));
+    h->tc.xt = h->xt;
+  }
   const int lists_max = std::max(h->grid_simt, h->grid_tc * remoe::kTcMaxStatesPerCta);
   const size_t cand_lanes = std::max((size_t)h->grid_simt * 32,
                                      (size_t)h->grid_tc * h->tc.threads_per_cta_queries);
@@ -315,8 +328,10 @@ static remoe_status_t build_impl(remoe_sps* h, const uint16_t* emb, const float*
   // ---- seeding sample: S rows j * stride, S a multiple
   // of 128, only for large shards.  The sample is read in place through a strided tensor
   // map; only its norms and global ids are copied.
+  int64_t seed_stride = remoe::kSeedStride;
+  if (const char* e = getenv("REMOE_SEED_STRIDE")) seed_stride = std::max(2, atoi(e));
   if (h->tc.ok && c.n_local >= 32 * 2048) {
-    const int64_t stride = std::min<int64_t>(16, c.n_local / 2048);
+    const int64_t stride = std::min<int64_t>(seed_stride, c.n_local / 2048);
     const int64_t S = (c.n_local / stride) / 128 * 128;
     h->seed_rows = S;
     ST_TRY(h->alloc((void**)&h->xns, (size_t)S * 4));
@@ -331,6 +346,8 @@ static remoe_status_t build_impl(remoe_sps* h, const uint16_t* emb, const float*
     if (!h->tc_seed.ok) h->seed_rows = 0;
   }
   if (const char* e = getenv("REMOE_SEED")) h->seed_mode = atoi(e) != 0 ? 1 : 0;
+  if (const char* e = getenv("REMOE_SEED_MIN_B")) h->seed_min_b = atoi(e);
+  if (const char* e = getenv("REMOE_SEED_KS")) h->seed_ks = std::max(0, std::min(32, atoi(e)));
   if (const char* e = getenv("REMOE_PAIR_MIN_B")) h->pair_min_b = atoi(e);
   ST_TRY(h->alloc((void**)&h->cand_buf, cand_lanes * capmax * 8));
   ST_TRY(h->alloc((void**)&h->lists, (size_t)mb * lists_max * c.max_k * 8));
@@ -446,12 +463,20 @@ static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k
     }
   } else {
     int nl = 0;
-    const bool seed = h->seed_mode == 1 || (h->seed_mode == -1 && k > 32);
-    if (h->seed_rows > 0 && seed && 8 * k <= h->seed_rows) {
-      // Scan the sample with the register top-k (k_s = min(k, 32) per state): the k-th best
-      // key of the union of the per-state lists is a real key of the store, hence a lower
-      // bound of the final k-th best; minus one it seeds the thresholds (strict bound).
-      const int ks = std::min(k, 32);
+    const bool seed = h->seed_mode == 1 || (h->seed_mode == -1 && (k > 32 || bc >= h->seed_min_b));
+    // Lists per query the seed scan will produce, at least: one per CTA of a query slab
+    // (M >= 64 queries per slab) or per CTA pair of a 256-query group.
+    const int sg = h->tc_seed.grid;
+    const int lists_min = which == 3 ? std::max(1, (sg / 2) / std::max(1, std::min((bc + 255) / 256, sg / 2)))
+                                     : std::max(1, sg / std::max(1, std::min((bc + 63) / 64, sg)));
+    int ks_auto = remoe::seed_ks_for(k);
+    while (ks_auto < 32 && (int64_t)lists_min * ks_auto < 4 * k) ks_auto *= 2;
+    const int ks = h->seed_ks > 0 ? std::min(h->seed_ks, k) : std::min(ks_auto, k);
+    if (h->seed_rows > 0 && seed && 8 * k <= h->seed_rows && (int64_t)lists_min * ks >= k) {
+      // Scan the sample with a short register top-k (k_s keys per state, k_s = 1 for
+      // k <= 32: a running max, no insertion work): the k-th best key of the union of the
+      // per-CTA lists is a real key of the store, hence a lower bound of the final k-th
+      // best; minus one it seeds the thresholds (strict bound).
       int sl = 0;
       const remoe_status_t ss =
           which == 3 ? remoe::tc_pair_scan(&h->tc_seed, q, h->qnorm, bc, ks, c.sigma, h->xns, h->seed_rows, 0,

@@ -1,6 +1,8 @@
 // tc_host.h -- host side of the tensor-core (tcgen05) scan: plan + launch.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <stdlib.h>
 #include <stdint.h>
 
 #include "remoe.h"
@@ -9,6 +11,26 @@ namespace remoe {
 
 // Batches up to this size use the streaming CUDA-core scan when both are legal.
 constexpr int kSimtMaxB = 0;  // the tensor-core scan is faster at every measured B (profiles/)
+
+// Threshold seeding (runtime.cu): batches >= kSeedMinB (and every k > 32) first scan every
+// kSeedStride-th row with a k_s-key register top-k per state.
+constexpr int kSeedMinB = 32;
+constexpr int kSeedStride = 64;
+// L2 promotion of the store's TMA boxes (128 B per row per box); REMOE_TC_PROMO = 0 none,
+// 1 64 B, 2 128 B, 3 256 B.
+inline CUtensorMapL2promotion tmap_promotion() {
+  const char* e = getenv("REMOE_TC_PROMO");
+  const int v = e ? atoi(e) : 3;
+  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+       : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+       : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+// K-block visiting order of the tensor-core scans (tcgen05.cuh kb_at); REMOE_TC_KB_ORDER.
+inline int kb_order_env() {
+  const char* e = getenv("REMOE_TC_KB_ORDER");
+  return e ? atoi(e) : 0;
+}
+inline int seed_ks_for(int k) { return k <= 32 ? 1 : k <= 64 ? 2 : 4; }
 
 struct TcPlan {
   bool ok = false;            // tensor-core scan usable for this store
@@ -19,7 +41,16 @@ struct TcPlan {
   const uint16_t* x = nullptr;
   int64_t n_rows = 0;
   int dim = 0;
+  int64_t row_stride = 0;     // elements between rows
+  // Tiled copy of the store (tc_tile_store), or nullptr: box (tile, kb) = 128 rows x 64
+  // elements, pre-swizzled (SWIZZLE_128B) and contiguous, 16 KB at xt + (tile*nkb + kb)*8192.
+  const uint16_t* xt = nullptr;
 };
+
+// Writes the tiled, pre-swizzled copy of x [n_rows x dim] (dim % 64 == 0) into xt
+// [ceil(n_rows/128) * 128 * dim] (rows past n_rows are zero).
+cudaError_t tc_tile_store(const uint16_t* x, int64_t n_rows, int dim, uint16_t* xt, cudaStream_t st);
+inline size_t tc_tiled_bytes(int64_t n_rows, int dim) { return (size_t)((n_rows + 127) / 128) * 128 * dim * 2; }
 
 // row_stride: elements between consecutive rows (default dim; a multiple of dim selects
 // every (row_stride/dim)-th row of the store, e.g. the threshold-seeding sample).
