@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
 // ------------------------------------------------------------------ host side
 
 static size_t pair_smem(int nst, int buf_bytes) {
-  return 1024 + (size_t)nst * 2 * kBox + (2 * (size_t)nst + 2 * kPAcc + 2) * 8 + kPEpiWarps * kPairN * 4 +
+  return (size_t)dyn_smem_pad() + (size_t)nst * 2 * kBox + (2 * (size_t)nst + 2 * kPAcc + 2) * 8 + kPEpiWarps * kPairN * 4 +
          kQPerCta * 8 + (size_t)buf_bytes;
 }
 

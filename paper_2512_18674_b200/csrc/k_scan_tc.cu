@@ -89,10 +89,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* cempty = bars + 2 * NST + 2 * kAcc;  // [NST] cluster-wide "slot free" (leader CTA)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NST + 2 * kAcc);
   // [8 warps][128] x-norms, 16-byte aligned for ld/st.shared.v4
+  // [2 parities][2 buffers][128] tile x-norms, shared by the 4 warps of a parity
   float* sXn = reinterpret_cast<float*>(bars + ((3 * NST + 2 * kAcc + 2 + 1) & ~1));
   // [128] per-query threshold shared by the two parity states of the CTA (register top-k)
-  unsigned long long* pair_thr = reinterpret_cast<unsigned long long*>(sXn + kEpiWarps * kTileN);
-  uint64_t* sBuf = reinterpret_cast<uint64_t*>(pair_thr + 128);  // [256][CAP] if p.smem_bufs
+  unsigned long long* pair_thr = reinterpret_cast<unsigned long long*>(sXn + 4 * kTileN);  // [M]
+  uint64_t* sBuf = reinterpret_cast<uint64_t*>(pair_thr + M);  // [256][CAP] if p.smem_bufs
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -126,7 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&cempty[s], C);
     }
     for (int s = 0; s < kAcc; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
-    for (int s = 0; s < 128; ++s) pair_thr[s] = 0ull;
+    for (int s = 0; s < M; ++s) pair_thr[s] = 0ull;
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_x) : "memory");
   }
@@ -246,7 +247,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     pdl_wait();  // k_norms: query norms and zeroed shared thresholds
     const float qn = active ? qnorm_sl[m] : 0.f;
     const int slot = e * 32 + lane;
-    float* xs = sXn + e * kTileN;  // this warp's copy of the tile's |x_j|
+    // the tile's |x_j|: one copy per parity, double buffered by iteration.  Written after
+    // the tile's accumulator wait: by then every warp of the parity has released the
+    // accumulator of tile i - 4, i.e. has finished with the buffer being overwritten.
+    float* xs_base = sXn + parity * 2 * kTileN;
     constexpr int kCap = 32 * (P > 0 ? P : 2);
     uint64_t* buf = p.smem_bufs ? sBuf + (size_t)slot * kCap
                                 : p.cand_buf + (cta_lin * kTcEpilogueThreads + slot) * kCap;
@@ -283,13 +287,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nvalid = (int)((p.n_rows - row0) < kTileN ? (p.n_rows - row0) : kTileN);
       const float4 xv = xv_next;
       const uint64_t gt = gt_next;
-      __syncwarp();
-      reinterpret_cast<float4*>(xs)[lane] = xv;
-      __syncwarp();
       xv_next = load_xn(t + tstep);
       gt_next = tk.peek_shared();
       if (p.epi_sleep) mbar_wait_sleep(&tfull[acc], aph);
       else mbar_wait(&tfull[acc], aph);
+      float* xs = xs_base + ((i >> 1) & 1) * kTileN;
+      reinterpret_cast<float4*>(xs)[lane] = xv;  // the 4 warps write identical values
+      asm volatile("bar.sync %0, 128;" ::"r"(7 + parity) : "memory");  // the parity's 4 warps
       if (active) tk.raise(gt);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kTileN);
@@ -306,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (KR > 0) {
           // the other parity state of this query lives in the same CTA: share its k-th best
           // through shared memory every chunk (exact: disjoint rows, own k-th best keys)
-          if (active) tk.raise(*reinterpret_cast<volatile unsigned long long*>(pair_thr + quarter * 32 + lane));
+          if (active) tk.raise(*reinterpret_cast<volatile unsigned long long*>(pair_thr + m));
         }
         const float* xc = xs + c * 32;
         unsigned mask = 0;
@@ -345,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
             if (active && tk.thr > pair_pub) {
-              atomicMax(pair_thr + quarter * 32 + lane, (unsigned long long)tk.thr);
+              atomicMax(pair_thr + m, (unsigned long long)tk.thr);
               pair_pub = tk.thr;
             }
           }
@@ -454,9 +458,36 @@ cudaError_t tc_tile_store(const uint16_t* x, int64_t n_rows, int dim, uint16_t* 
 
 // ------------------------------------------------------------------ host side
 
+// Offset of dynamic shared memory from a 1024-byte boundary (kernels without static shared
+// memory): probed once; the scans align their base up to 1024, so they reserve 1024 bytes
+// of slack only if the base is not already aligned (the slack is worth a stage at D=1024).
+__global__ void k_probe_dyn_smem(unsigned* out) {
+  extern __shared__ uint8_t s_probe[];
+  if (threadIdx.x == 0) *out = smem_u32(s_probe) & 1023u;
+}
+
+int dyn_smem_pad() {
+  static int pad = -1;
+  if (pad >= 0) return pad;
+  int result = 1024;
+  unsigned* d = nullptr;
+  unsigned h = 1;
+  const int bytes = kMaxSmem - 4096;
+  if (cudaFuncSetAttribute((const void*)k_probe_dyn_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) ==
+          cudaSuccess &&
+      cudaMalloc(&d, sizeof(unsigned)) == cudaSuccess) {
+    k_probe_dyn_smem<<<1, 32, bytes>>>(d);
+    if (cudaMemcpy(&h, d, sizeof(unsigned), cudaMemcpyDeviceToHost) == cudaSuccess && h == 0) result = 0;
+    cudaFree(d);
+  }
+  cudaGetLastError();
+  pad = result;
+  return pad;
+}
+
 static size_t tc_smem(int M, int D, int nst, int buf_bytes) {
-  return 1024 + (size_t)(D / kBlockK) * M * 128 + (size_t)nst * kStageBytes +
-         (3 * (size_t)nst + 2 * kAcc + 4) * 8 + kEpiWarps * kTileN * 4 + 128 * 8 + (size_t)buf_bytes;
+  return (size_t)dyn_smem_pad() + (size_t)(D / kBlockK) * M * 128 + (size_t)nst * kStageBytes +
+         (3 * (size_t)nst + 2 * kAcc + 4) * 8 + 4 * kTileN * 4 + (size_t)M * 8 + (size_t)buf_bytes;
 }
 
 static int tc_stages(int M, int D, int buf_bytes) {

@@ -50,6 +50,8 @@ struct TcPlan {
 // Writes the tiled, pre-swizzled copy of x [n_rows x dim] (dim % 64 == 0) into xt
 // [ceil(n_rows/128) * 128 * dim] (rows past n_rows are zero).
 cudaError_t tc_tile_store(const uint16_t* x, int64_t n_rows, int dim, uint16_t* xt, cudaStream_t st);
+// 0 if dynamic shared memory starts 1024-byte aligned, else 1024 (probed once per process).
+int dyn_smem_pad();
 inline size_t tc_tiled_bytes(int64_t n_rows, int dim) { return (size_t)((n_rows + 127) / 128) * 128 * dim * 2; }
 
 // row_stride: elements between consecutive rows (default dim; a multiple of dim selects
