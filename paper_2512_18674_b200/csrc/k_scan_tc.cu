@@ -27,6 +27,8 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include <vector>
+
 #include "host_util.h"
 #include "kernels.h"
 #include "tc_host.h"
@@ -65,12 +67,24 @@ struct TcArgs {
   int epi_sleep;           // epilogue waits with a suspend-time hint (REMOE_EPI_SLEEP=1)
   const uint16_t* xt;      // tiled store (TcPlan::xt): 1-D bulk copies, else the tensor map
   int kb_order;            // K-block visiting order (kb_at)
+  unsigned long long* trace;  // REMOE_TC_TRACE: [grid][16] globaltimer stamps
   unsigned long long* stats;  // REMOE_TC_STATS: [0] candidate columns, [1] inserts, [2] chunks with a candidate
 };
 }  // namespace
 
 // M = queries per pass (UMMA M, 64 or 128).  For M = 64 the accumulator rows live in
-// lanes 0-15 of each 32-lane TMEM quarter (row m -> lane 32*(m/16) + m%16).
+// lanes 0-15 of each 32-lane TMEM quarter (row r -> lane 32*(r/16) + r%16).  Slab row
+// r = R*q + l (R = M/4 rows per quarter) holds query m = 4*l + q, so a batch smaller than
+// M spreads over all four epilogue quarters instead of filling the first one.
+#define TRACE(idx)                                                                              \
+  do {                                                                                          \
+    if (p.trace && (threadIdx.x & 31) == 0) {                                                   \
+      unsigned long long t_;                                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                    \
+      p.trace[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + (idx)] = t_;                         \
+    }                                                                                           \
+  } while (0)
+
 template <int M, int P, int KR>
 __global__ void __launch_bounds__(kThreads, 1)
     k_scan_tc(const __grid_constant__ CUtensorMap tmap_x, TcArgs p) {
@@ -98,6 +112,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t n_tiles = (p.n_rows + kTileN - 1) / kTileN;
+  TRACE(0);
   pdl_trigger();  // the merge kernel may be scheduled as SMs free up
   // Query slab of this CTA (blockIdx.y).  With several slabs, the CTAs of every slab walk
   // the store tiles in the same order (tile = blockIdx.x + j * gridDim.x), so the slabs
@@ -142,6 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  TRACE(1);
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (warp != 0) {
@@ -150,10 +166,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int chunks = M * (D / 8);
     const uint32_t a_s = smem_u32(sA);
     for (int i = threadIdx.x - 32; i < chunks; i += blockDim.x - 32) {
-      const int m = i / (D / 8);
-      const int cc = i - m * (D / 8);
+      const int r = i / (D / 8);  // slab row
+      const int m = 4 * (r % (M / 4)) + r / (M / 4);  // its query
+      const int cc = i - r * (D / 8);
       const int kb = cc >> 3, c = cc & 7;
-      const uint32_t dst = a_s + (uint32_t)(kb * M * 128 + m * 128 + ((c ^ (m & 7)) << 4));
+      const uint32_t dst = a_s + (uint32_t)(kb * M * 128 + r * 128 + ((c ^ (r & 7)) << 4));
       const uint16_t* src = qsl + (size_t)(m < nq ? m : 0) * D + cc * 8;
       const uint32_t bytes = m < nq ? 16u : 0u;  // src-size 0 -> zero fill
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes)
@@ -162,6 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("cp.async.wait_all;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("bar.sync 1, %0;" ::"n"(kThreads - 32) : "memory");  // warps 1-9 only
+    TRACE(2);
   }
 
   if (warp == 0) {
@@ -212,6 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = it % NST;
           const uint32_t ph = (uint32_t)(it / NST) & 1u;
           mbar_wait(&full[s], ph);
+          if (it == 0) TRACE(4);
           tc_fence_after();
           const uint32_t abase = a0 + (uint32_t)(kb * M * 128);
           const uint32_t bbase = b0 + (uint32_t)(s * kStageBytes);
@@ -223,6 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (C > 1) umma_commit_mc(&cempty[s], 1);  // the leader's slot-free barrier
         }
         umma_commit(&tfull[acc]);
+        if (i == 0) TRACE(5);
       }
     }
   } else {
@@ -242,9 +262,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int e = warp - 2;
     const int quarter = warp & 3;
     const int parity = e >> 2;
-    const int m = (M == 128) ? quarter * 32 + lane : quarter * 16 + lane;
+    const int m = 4 * lane + quarter;  // slab row R*quarter + lane (see the slab load)
     const bool active = (M == 128 || lane < 16) && m < nq;
     pdl_wait();  // k_norms: query norms and zeroed shared thresholds
+    TRACE(6);
     const float qn = active ? qnorm_sl[m] : 0.f;
     const int slot = e * 32 + lane;
     // the tile's |x_j|: one copy per parity, double buffered by iteration.  Written after
@@ -294,6 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float* xs = xs_base + ((i >> 1) & 1) * kTileN;
       reinterpret_cast<float4*>(xs)[lane] = xv;  // the 4 warps write identical values
       asm volatile("bar.sync %0, 128;" ::"r"(7 + parity) : "memory");  // the parity's 4 warps
+      if (i < 2) TRACE(7);
       if (active) tk.raise(gt);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kTileN);
@@ -395,6 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if constexpr (KR > 0) tk.publish();
     }
+    TRACE(8);
     if (KR > 0 && p.merge_in_cta) {
       // Merge the two parity states of each query inside the CTA (one list per CTA per
       // query halves the merge kernel's input).  The TMA stage ring is idle now (every
@@ -423,6 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   __syncthreads();
+  TRACE(9);
   if (C > 1) {  // no CTA leaves while a peer may still arrive on its barriers
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
@@ -642,9 +666,34 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
       cudaMemsetAsync(stats, 0, 3 * 8, st);
       a.stats = stats;
     }
+    static unsigned long long* trace = nullptr;
+    const int n_cta = ctas_per_slab * ns;
+    if (getenv("REMOE_TC_TRACE")) {  // debug: per-CTA globaltimer stamps of the launch phases
+      if (!trace) cudaMalloc(&trace, (size_t)148 * 64 * 16 * 8);
+      cudaMemsetAsync(trace, 0, (size_t)n_cta * 16 * 8, st);
+      a.trace = trace;
+    }
     const dim3 g((unsigned)ctas_per_slab, (unsigned)ns);
     cudaError_t e = (M == 128) ? launch_tc_m<128>(t, a, g, st) : launch_tc_m<64>(t, a, g, st);
     if (e != cudaSuccess) return REMOE_ERR_CUDA;
+    if (a.trace) {
+      std::vector<unsigned long long> h((size_t)n_cta * 16);
+      cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      unsigned long long t0 = ~0ull;
+      for (int c = 0; c < n_cta; ++c) if (h[c * 16] && h[c * 16] < t0) t0 = h[c * 16];
+      fprintf(stderr, "[remoe] tc trace (us from first CTA start; CTA 0 | max over CTAs): nq %d k %d tiles %lld\n",
+              a.nq, k, (long long)((n_rows + kTileN - 1) / kTileN));
+      const char* names[10] = {"start", "setup", "slab", "-", "mma first full", "mma tile0 commit", "epi pdl_wait",
+                               "epi first tfull", "epi loop done", "end"};
+      for (int i = 0; i < 10; ++i) {
+        if (i == 3) continue;
+        unsigned long long mx = 0;
+        for (int c = 0; c < n_cta; ++c) if (h[c * 16 + i] > mx) mx = h[c * 16 + i];
+        fprintf(stderr, "  %-18s %9.2f | %9.2f\n", names[i], h[i] ? (h[i] - t0) / 1e3 : -1.0,
+                mx ? (mx - t0) / 1e3 : -1.0);
+      }
+    }
     if (a.stats) {
       unsigned long long h[3];
       cudaMemcpyAsync(h, a.stats, 24, cudaMemcpyDeviceToHost, st);
