@@ -463,7 +463,9 @@ static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k
     }
   } else {
     int nl = 0;
-    const bool seed = h->seed_mode == 1 || (h->seed_mode == -1 && (k > 32 || bc >= h->seed_min_b));
+    const int seed_min_b = c.n_local < remoe::kSeedSmallRows ? std::min(h->seed_min_b, remoe::kSeedMinBSmall)
+                                                              : h->seed_min_b;
+    const bool seed = h->seed_mode == 1 || (h->seed_mode == -1 && (k > 32 || bc >= seed_min_b));
     // Lists per query the seed scan will produce, at least: one per CTA of a query slab
     // (M >= 64 queries per slab) or per CTA pair of a 256-query group.
     const int sg = h->tc_seed.grid;

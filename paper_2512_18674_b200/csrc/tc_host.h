@@ -15,6 +15,10 @@ constexpr int kSimtMaxB = 0;  // the tensor-core scan is faster at every measure
 // Threshold seeding (runtime.cu): batches >= kSeedMinB (and every k > 32) first scan every
 // kSeedStride-th row with a k_s-key register top-k per state.
 constexpr int kSeedMinB = 32;
+// Shards below kSeedSmallRows rows give each top-k state so few rows that the warm-up
+// inserts dominate: seed from kSeedMinBSmall queries on (measured on the c2 store).
+constexpr int64_t kSeedSmallRows = 512 * 1024;
+constexpr int kSeedMinBSmall = 8;
 constexpr int kSeedStride = 64;
 // L2 promotion of the store's TMA boxes (128 B per row per box); REMOE_TC_PROMO = 0 none,
 // 1 64 B, 2 128 B, 3 256 B.

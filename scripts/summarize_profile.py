@@ -54,7 +54,10 @@ def full_metrics(rep):
     r = list(csv.reader(io.StringIO(out)))
     if len(r) < 3:
         return {}
-    h, u, v = r[0], r[1], r[2]
+    h, u = r[0], r[1]
+    # several captured launches (e.g. the threshold-seeding scan and the main scan): keep the longest
+    it = h.index("gpu__time_duration.sum")
+    v = max(r[2:], key=lambda row: float(row[it].replace(",", "") or 0))
     res = OrderedDict()
     for name in KEY_METRICS:
         if name in h:
