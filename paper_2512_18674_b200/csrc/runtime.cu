@@ -111,10 +111,14 @@ struct remoe_sps {
   remoe::TcPlan tc{};
   // threshold seeding: a strided sample of S rows, scanned first; its
   // k-th best key - 1 is a strict lower bound that the full scan starts from
-  remoe::TcPlan tc_seed{};
-  int64_t seed_rows = 0;
-  float* xns = nullptr;
-  int64_t* gids = nullptr;
+  struct SeedSample {
+    int64_t stride = 0, rows = 0;  // rows j * stride, j < rows
+    remoe::TcPlan tc{};            // strided tensor map over the store
+    float* xns = nullptr;          // their norms
+    int64_t* gids = nullptr;       // their global ids
+  };
+  SeedSample seeds[4];  // strides 64, 32, 16, 8 (larger k takes a denser sample)
+  int n_seeds = 0;
   uint64_t* seed_top = nullptr;
   // -1 auto: seed when k > 32 or B >= seed_min_b; 1 always (REMOE_SEED=1); 0 never
   // (REMOE_SEED=0).  Without a seed every top-k state (a CTA's rows for one query) starts
@@ -182,7 +186,8 @@ struct remoe_sps {
     for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
     prof_ev.clear();
     remoe::tc_plan_destroy(&tc);
-    remoe::tc_plan_destroy(&tc_seed);
+    for (int i = 0; i < n_seeds; ++i) remoe::tc_plan_destroy(&seeds[i].tc);
+    n_seeds = 0;
     if (has_tree) { remoe::tree_free(&tree); has_tree = false; }
     if (comm) { ncclCommDestroy(comm); comm = nullptr; }
   }
@@ -328,22 +333,28 @@ static remoe_status_t build_impl(remoe_sps* h, const uint16_t* emb, const float*
   // ---- seeding sample: S rows j * stride, S a multiple
   // of 128, only for large shards.  The sample is read in place through a strided tensor
   // map; only its norms and global ids are copied.
-  int64_t seed_stride = remoe::kSeedStride;
-  if (const char* e = getenv("REMOE_SEED_STRIDE")) seed_stride = std::max(2, atoi(e));
+  std::vector<int64_t> strides = {remoe::kSeedStride, remoe::kSeedStride / 2, remoe::kSeedStride / 4,
+                                  remoe::kSeedStride / 8};
+  if (const char* e = getenv("REMOE_SEED_STRIDE")) strides = {std::max(2, atoi(e))};
   if (h->tc.ok && c.n_local >= 32 * 2048) {
-    const int64_t stride = std::min<int64_t>(seed_stride, c.n_local / 2048);
-    const int64_t S = (c.n_local / stride) / 128 * 128;
-    h->seed_rows = S;
-    ST_TRY(h->alloc((void**)&h->xns, (size_t)S * 4));
-    ST_TRY(h->alloc((void**)&h->gids, (size_t)S * 8));
     ST_TRY(h->alloc((void**)&h->seed_top, (size_t)mb * c.max_k * 8));
-    CUDA_TRY(cudaMemcpy2DAsync(h->xns, 4, h->xnorm, (size_t)stride * 4, 4, S, cudaMemcpyDeviceToDevice, st));
-    std::vector<int64_t> g(S);
-    for (int64_t j = 0; j < S; ++j) g[j] = c.global_offset + j * stride;
-    CUDA_TRY(cudaMemcpyAsync(h->gids, g.data(), S * 8, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    ST_TRY(remoe::tc_plan_create(&h->tc_seed, h->x, S, c.dim, h->num_sms, c.max_k, stride * c.dim));
-    if (!h->tc_seed.ok) h->seed_rows = 0;
+    for (int64_t want : strides) {
+      const int64_t stride = std::max<int64_t>(2, std::min<int64_t>(want, c.n_local / 2048));
+      if (h->n_seeds > 0 && h->seeds[h->n_seeds - 1].stride == stride) continue;
+      remoe_sps::SeedSample& sd = h->seeds[h->n_seeds];
+      const int64_t S = (c.n_local / stride) / 128 * 128;
+      sd.stride = stride;
+      sd.rows = S;
+      ST_TRY(h->alloc((void**)&sd.xns, (size_t)S * 4));
+      ST_TRY(h->alloc((void**)&sd.gids, (size_t)S * 8));
+      CUDA_TRY(cudaMemcpy2DAsync(sd.xns, 4, h->xnorm, (size_t)stride * 4, 4, S, cudaMemcpyDeviceToDevice, st));
+      std::vector<int64_t> g(S);
+      for (int64_t j = 0; j < S; ++j) g[j] = c.global_offset + j * stride;
+      CUDA_TRY(cudaMemcpyAsync(sd.gids, g.data(), S * 8, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      ST_TRY(remoe::tc_plan_create(&sd.tc, h->x, S, c.dim, h->num_sms, c.max_k, stride * c.dim));
+      if (sd.tc.ok) ++h->n_seeds;
+    }
   }
   if (const char* e = getenv("REMOE_SEED")) h->seed_mode = atoi(e) != 0 ? 1 : 0;
   if (const char* e = getenv("REMOE_SEED_MIN_B")) h->seed_min_b = atoi(e);
@@ -468,23 +479,33 @@ static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k
     const bool seed = h->seed_mode == 1 || (h->seed_mode == -1 && (k > 32 || bc >= seed_min_b));
     // Lists per query the seed scan will produce, at least: one per CTA of a query slab
     // (M >= 64 queries per slab) or per CTA pair of a 256-query group.
-    const int sg = h->tc_seed.grid;
+    // Sample density by k: the sample should hold ~k rows of a query's topic for its k-th
+    // best to approach the final k-th best (stride 64 for k <= 16, 8 for k >= 128).
+    int want_stride = remoe::kSeedStride;
+    while (want_stride > remoe::kSeedStride / 8 && (int64_t)want_stride * k > 1024) want_stride /= 2;
+    int si = 0;
+    for (int i = 0; i < h->n_seeds; ++i)
+      if (h->seeds[i].stride >= want_stride) si = i;
+    const remoe_sps::SeedSample* sd = h->n_seeds > 0 ? &h->seeds[si] : nullptr;
+    const int sg = sd ? sd->tc.grid : 0;
     const int lists_min = which == 3 ? std::max(1, (sg / 2) / std::max(1, std::min((bc + 255) / 256, sg / 2)))
                                      : std::max(1, sg / std::max(1, std::min((bc + 63) / 64, sg)));
     int ks_auto = remoe::seed_ks_for(k);
     while (ks_auto < 32 && (int64_t)lists_min * ks_auto < 4 * k) ks_auto *= 2;
     const int ks = h->seed_ks > 0 ? std::min(h->seed_ks, k) : std::min(ks_auto, k);
-    if (h->seed_rows > 0 && seed && 8 * k <= h->seed_rows && (int64_t)lists_min * ks >= k) {
+    if (sd && seed && 8 * k <= sd->rows && (int64_t)lists_min * ks >= k) {
       // Scan the sample with a short register top-k (k_s keys per state, k_s = 1 for
       // k <= 32: a running max, no insertion work): the k-th best key of the union of the
       // per-CTA lists is a real key of the store, hence a lower bound of the final k-th
       // best; minus one it seeds the thresholds (strict bound).
       int sl = 0;
       const remoe_status_t ss =
-          which == 3 ? remoe::tc_pair_scan(&h->tc_seed, q, h->qnorm, bc, ks, c.sigma, h->xns, h->seed_rows, 0,
-                                           h->gids, h->cand_buf, h->gthr + c.max_batch, h->lists, st, &nl, &sl)
-                     : remoe::tc_scan(&h->tc_seed, q, h->qnorm, bc, ks, c.sigma, h->xns, h->seed_rows, 0, h->gids,
-                                      h->cand_buf, h->gthr + c.max_batch, h->lists, st, &nl, &sl);
+          which == 3 ? remoe::tc_pair_scan(const_cast<remoe::TcPlan*>(&sd->tc), q, h->qnorm, bc, ks, c.sigma, sd->xns,
+                                           sd->rows, 0, sd->gids, h->cand_buf, h->gthr + c.max_batch, h->lists, st,
+                                           &nl, &sl)
+                     : remoe::tc_scan(const_cast<remoe::TcPlan*>(&sd->tc), q, h->qnorm, bc, ks, c.sigma, sd->xns,
+                                      sd->rows, 0, sd->gids, h->cand_buf, h->gthr + c.max_batch, h->lists, st, &nl,
+                                      &sl);
       if (ss != REMOE_OK)
         return fail(ss, "seed scan launch failed: %s", cudaGetErrorString(cudaGetLastError()));
       if ((int64_t)sl * ks < k) return fail(REMOE_ERR_STATE, "seed sample too small for k=%d", k);
