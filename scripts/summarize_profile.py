@@ -116,7 +116,8 @@ def main():
         tpath = os.path.join(dst, "traffic.json")
         tj = json.load(open(tpath)) if os.path.exists(tpath) else {}
         c = bench["config"]
-        kern = 2 if "tc" in c.get("scan_kernel", "") else 1
+        sk = c.get("scan_kernel", "")
+        kern = 3 if "pair" in sk else 2 if "tc" in sk else 1
         tj[f"c{c['workload'].split(':')[0][1:]}:B{c['batch']}:k{c['k']}:G{bench['n_gpus']}:{kern}"] = traffic
         json.dump(tj, open(tpath, "w"), indent=1, sort_keys=True)
     with open(os.path.join(dst, f"{rnd}_{tag}_summary.md"), "w") as f:
