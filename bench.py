@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--kernel", default="auto", choices=["auto", "stream", "tc", "pair"])
     ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-scan-events", action="store_true",
+                    help="debug: no per-scan CUDA events inside the timed steps (no roofline)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
@@ -246,7 +248,7 @@ def run_ours(args):
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     clocks = ClockSampler(local)
     clocks.start()
-    sps.profile(True)
+    sps.profile(not args.no_scan_events)
     launches_before = 0
     barrier()
     torch.cuda.synchronize(dev)
@@ -297,7 +299,7 @@ def run_ours(args):
     info = sps.info()
     kern = {1: "k_scan_simt (CUDA cores, TMA bulk staging)", 2: "k_scan_tc (tcgen05 + TMA)",
             3: "k_scan_pair (tcgen05 cta_group::2 + TMA)"}.get(info.last_scan_kernel, "?")
-    per_launch_ms = scan_ms_max / max(1, scan_launches)
+    per_launch_ms = max(scan_ms_max / max(1, scan_launches), 1e-9)
     nq_per_launch = B / max(1, scan_launches // max(1, args.steps))
     alg = algorithmic_bytes_per_launch(n_loc, cfg.dim, nq_per_launch)
     peaks = {}
