@@ -45,6 +45,7 @@ constexpr int kEpiWarps = 8;
 constexpr int kAcc = 4;              // TMEM accumulator stages
 constexpr int kTmemCols = kAcc * kTileN;
 constexpr int kMaxSmem = 232448;     // 227 KB opt-in
+constexpr int kMaxStages = 8;        // stage ring depth cap (deeper rings measured no faster)
 
 struct TcArgs {
   const float* xnorm;
@@ -67,6 +68,9 @@ struct TcArgs {
   int epi_sleep;           // epilogue waits with a suspend-time hint (REMOE_EPI_SLEEP=1)
   const uint16_t* xt;      // tiled store (TcPlan::xt): 1-D bulk copies, else the tensor map
   int kb_order;            // K-block visiting order (kb_at)
+  int dbg;                 // REMOE_TC_DBG bits (experiments only; 1 = skip the MMA)
+  int slab_rows;           // query rows stored per K-block (multiple of 8, <= M): a single
+                           // slab of nq queries stores only ceil(nq/8) 8-row atoms
   unsigned long long* trace;  // REMOE_TC_TRACE: [grid][16] globaltimer stamps
   unsigned long long* stats;  // REMOE_TC_STATS: [0] candidate columns, [1] inserts, [2] chunks with a candidate
 };
@@ -94,7 +98,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nkb = D / kBlockK;  // host guarantees D % 64 == 0
   const int NST = p.n_stages;
   uint8_t* sA = smem;                                   // [nkb][M rows][128 B] swizzled
-  uint8_t* sB = sA + (size_t)nkb * M * 128;             // [NST][128 rows][128 B]
+  const int SR = p.slab_rows;
+  uint8_t* sB = sA + (size_t)nkb * SR * 128;            // [NST][128 rows][128 B]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + (size_t)NST * kStageBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + NST;
@@ -162,15 +167,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
   if (warp != 0) {
     // Warps 1-9 write the resident query slab while warp 0 already streams the store:
-    // Q[m][kb*64 + c*8 .. +8] -> sA + kb*M*128 + m*128 + ((c ^ (m & 7)) * 16)  (SWIZZLE_128B)
-    const int chunks = M * (D / 8);
+    // Q[m][kb*64 + c*8 .. +8] -> sA + kb*SR*128 + m*128 + ((c ^ (m & 7)) * 16)  (SWIZZLE_128B).
+    // With SR < M the UMMA's rows SR .. M-1 read past the K-block (other K-blocks or the
+    // stage ring): garbage accumulator rows of queries >= nq, which no lane reads.
+    const int chunks = SR * (D / 8);
     const uint32_t a_s = smem_u32(sA);
     for (int i = threadIdx.x - 32; i < chunks; i += blockDim.x - 32) {
-      const int r = i / (D / 8);  // slab row
-      const int m = 4 * (r % (M / 4)) + r / (M / 4);  // its query
-      const int cc = i - r * (D / 8);
+      const int m = i / (D / 8);  // slab row = query
+      const int cc = i - m * (D / 8);
       const int kb = cc >> 3, c = cc & 7;
-      const uint32_t dst = a_s + (uint32_t)(kb * M * 128 + r * 128 + ((c ^ (r & 7)) << 4));
+      const uint32_t dst = a_s + (uint32_t)(kb * SR * 128 + m * 128 + ((c ^ (m & 7)) << 4));
       const uint16_t* src = qsl + (size_t)(m < nq ? m : 0) * D + cc * 8;
       const uint32_t bytes = m < nq ? 16u : 0u;  // src-size 0 -> zero fill
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes)
@@ -215,7 +221,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // kind::f16: D fp32 (bit 4), A bf16 (bits 7-9 = 1), B bf16 (bits 10-12 = 1),
       // both K-major, N >> 3 at bit 17, M >> 4 at bit 24
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTileN >> 3) << 17) |
+      // (debug REMOE_TC_DBG bit 4: N = 32, a quarter of the MMA work; wrong results)
+      const uint32_t nn = (p.dbg & 4) ? 32u : (uint32_t)kTileN;
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((nn >> 3) << 17) |
                              ((uint32_t)(M >> 4) << 24);
       const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
       int it = 0, i = 0;
@@ -232,8 +240,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&full[s], ph);
           if (it == 0) TRACE(4);
           tc_fence_after();
-          const uint32_t abase = a0 + (uint32_t)(kb * M * 128);
+          const uint32_t abase = a0 + (uint32_t)(kb * SR * 128);
           const uint32_t bbase = b0 + (uint32_t)(s * kStageBytes);
+          if (p.dbg & 1) {  // debug (REMOE_TC_DBG=1): no MMA, free the slot at once (wrong results)
+            mbar_arrive(&empty[s]);
+            continue;
+          }
 #pragma unroll
           for (int kk = 0; kk < kBlockK / 16; ++kk)
             umma_bf16(d_tmem, umma_desc(abase + kk * 32), umma_desc(bbase + kk * 32), idesc,
@@ -262,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int e = warp - 2;
     const int quarter = warp & 3;
     const int parity = e >> 2;
-    const int m = 4 * lane + quarter;  // slab row R*quarter + lane (see the slab load)
+    const int m = (M == 128) ? quarter * 32 + lane : quarter * 16 + lane;
     const bool active = (M == 128 || lane < 16) && m < nq;
     pdl_wait();  // k_norms: query norms and zeroed shared thresholds
     TRACE(6);
@@ -319,6 +331,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (active) tk.raise(gt);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kTileN);
+      if (p.dbg & 2) {  // debug (REMOE_TC_DBG=2): release the accumulator unread (wrong results)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        continue;
+      }
 #pragma unroll 1
       for (int c = 0; c < kTileN / 32; ++c) {
         uint32_t v[32];
@@ -509,15 +526,16 @@ int dyn_smem_pad() {
   return pad;
 }
 
-static size_t tc_smem(int M, int D, int nst, int buf_bytes) {
-  return (size_t)dyn_smem_pad() + (size_t)(D / kBlockK) * M * 128 + (size_t)nst * kStageBytes +
+// slab_rows: query rows stored per K-block (M for a full slab).
+static size_t tc_smem(int M, int slab_rows, int D, int nst, int buf_bytes) {
+  return (size_t)dyn_smem_pad() + (size_t)(D / kBlockK) * slab_rows * 128 + (size_t)nst * kStageBytes +
          (3 * (size_t)nst + 2 * kAcc + 4) * 8 + 4 * kTileN * 4 + (size_t)M * 8 + (size_t)buf_bytes;
 }
 
-static int tc_stages(int M, int D, int buf_bytes) {
-  const long avail = (long)kMaxSmem - (long)tc_smem(M, D, 0, buf_bytes);
+static int tc_stages(int M, int D, int buf_bytes, int slab_rows = 0) {
+  const long avail = (long)kMaxSmem - (long)tc_smem(M, slab_rows > 0 ? slab_rows : M, D, 0, buf_bytes);
   const long n = avail / (kStageBytes + 16);
-  return (int)(n > 8 ? 8 : n);
+  return (int)(n > kMaxStages ? kMaxStages : n);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -567,7 +585,7 @@ void tc_plan_destroy(TcPlan* t) { t->ok = false; }
 
 template <int M, int P, int KR = 0>
 static cudaError_t launch_tc_t(const TcPlan* t, const TcArgs& a, dim3 grid, cudaStream_t st) {
-  const size_t smem = tc_smem(M, a.dim, a.n_stages, a.smem_bufs ? kTcEpilogueThreads * 32 * P * 8 : 0);
+  const size_t smem = tc_smem(M, a.slab_rows, a.dim, a.n_stages, a.smem_bufs ? kTcEpilogueThreads * 32 * P * 8 : 0);
   static_assert(P >= 0, "P");
   auto kern = k_scan_tc<M, P, KR>;
   cudaError_t e = set_smem_attrs_once((const void*)kern, kMaxSmem);
@@ -623,8 +641,11 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
   // buffers go to shared memory when that still leaves >= 4 stages.
   const int M = tc_stages(128, t->dim, 0) >= 4 ? 128 : 64;
   const int buf_bytes = k <= 32 ? 0 : kTcEpilogueThreads * 32 * topk_P(k) * 8;
-  const bool smem_bufs = k > 32 && tc_stages(M, t->dim, buf_bytes) >= 4 && !getenv("REMOE_TC_GLOBAL_BUFS");
-  int nst = tc_stages(M, t->dim, smem_bufs ? buf_bytes : 0);
+  // a single slab stores only the 8-row atoms its queries need (more stages for small B)
+  const int n_slabs_all = (bc + M - 1) / M;
+  const int SR = (n_slabs_all == 1 && !getenv("REMOE_TC_FULL_SLAB")) ? ((bc + 7) / 8) * 8 : M;
+  const bool smem_bufs = k > 32 && tc_stages(M, t->dim, buf_bytes, SR) >= 4 && !getenv("REMOE_TC_GLOBAL_BUFS");
+  int nst = tc_stages(M, t->dim, smem_bufs ? buf_bytes : 0, SR);
   if (const char* e = getenv("REMOE_TC_STAGES")) { const int v = atoi(e); if (v >= 2 && v < nst) nst = v; }
   // register top-k merges its two parity states in-CTA when the stage ring can hold them
   const int KR = k <= 1 ? 1 : k <= 2 ? 2 : k <= 4 ? 4 : k <= 8 ? 8 : k <= 16 ? 16 : 32;
@@ -660,6 +681,8 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
     a.epi_sleep = getenv("REMOE_EPI_SLEEP") ? atoi(getenv("REMOE_EPI_SLEEP")) : 0;
     a.xt = t->xt;
     a.kb_order = kb_order_env();
+    a.slab_rows = SR;
+    a.dbg = getenv("REMOE_TC_DBG") ? atoi(getenv("REMOE_TC_DBG")) : 0;
     static unsigned long long* stats = nullptr;
     if (getenv("REMOE_TC_STATS")) {
       if (!stats) { cudaMalloc(&stats, 3 * 8); }
