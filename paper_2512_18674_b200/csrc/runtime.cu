@@ -137,6 +137,27 @@ struct remoe_sps {
   int last_launches = 0;
   size_t device_bytes = 0;
   std::vector<void*> allocs;
+  // CUDA graph of the host-buffer query (remoe_sps_query_host), one cached shape: the
+  // H2D copy, S1-S7 and the D2H copies replay as one launch; per call only the four
+  // memcpy nodes are re-pointed at the caller's (pinned) buffers.
+  struct HostGraph {
+    int B = -1, k = -1;
+    bool pred = false;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t h2d = nullptr, d2h_ids = nullptr, d2h_sc = nullptr, d2h_pred = nullptr;
+    int launches = 0;
+    void reset() {
+      if (exec) cudaGraphExecDestroy(exec);
+      if (graph) cudaGraphDestroy(graph);
+      exec = nullptr; graph = nullptr; B = -1; k = -1; pred = false;
+      h2d = d2h_ids = d2h_sc = d2h_pred = nullptr; launches = 0;
+    }
+  } hg;
+  // the graph is captured and replayed on a library stream (the caller's may be the legacy
+  // default stream, which cannot be captured), ordered after the caller's stream by an event
+  cudaStream_t gst = nullptr;
+  cudaEvent_t gev = nullptr;
   // live scan timing (remoe_sps_profile)
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;  // pairs (start, end)
@@ -181,6 +202,9 @@ struct remoe_sps {
     return REMOE_OK;
   }
   void release() {
+    hg.reset();
+    if (gev) { cudaEventDestroy(gev); gev = nullptr; }
+    if (gst) { cudaStreamDestroy(gst); gst = nullptr; }
     for (void* p : allocs) cudaFree(p);
     allocs.clear();
     for (cudaEvent_t e : prof_ev) cudaEventDestroy(e);
@@ -572,6 +596,81 @@ remoe_status_t remoe_sps_query(remoe_sps_t h, const uint16_t* q, int32_t B, int3
   return REMOE_OK;
 }
 
+static bool is_pinned(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// One batch (B <= max_batch, world == 1) through the cached CUDA graph; captured on the
+// first call of a (B, k, pred) shape.  Returns UNSUPPORTED (nothing enqueued) when a host
+// buffer is pageable, which stream capture cannot copy from.
+static remoe_status_t query_host_graph(remoe_sps* h, const uint16_t* q, int B, int k, int64_t* ids,
+                                       float* scores, float* pred, cudaStream_t st) {
+  if (!is_pinned(q) || !is_pinned(ids) || !is_pinned(scores) || !is_pinned(pred)) return REMOE_ERR_UNSUPPORTED;
+  const size_t qb = (size_t)B * h->cfg.dim * 2, ib = (size_t)B * k * 8, sb = (size_t)B * k * 4,
+               pb = (size_t)B * h->LE * 4;
+  auto& g = h->hg;
+  const cudaStream_t caller = st;
+  if (!h->gst) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->gst, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&h->gev, cudaEventDisableTiming));
+  }
+  st = h->gst;
+  CUDA_TRY(cudaEventRecord(h->gev, caller));  // after the caller's earlier work on the handle
+  CUDA_TRY(cudaStreamWaitEvent(st, h->gev, 0));
+  if (!(g.exec && g.B == B && g.k == k && g.pred == (pred != nullptr))) {
+    g.reset();
+    CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    int launches = 0;
+    cudaMemcpyAsync(h->hq, q, qb, cudaMemcpyHostToDevice, st);
+    const remoe_status_t qs = query_chunk(h, h->hq, B, k, h->hids, h->hscores, pred ? h->hpred : nullptr, st,
+                                          &launches);
+    cudaMemcpyAsync(ids, h->hids, ib, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(scores, h->hscores, sb, cudaMemcpyDeviceToHost, st);
+    if (pred) cudaMemcpyAsync(pred, h->hpred, pb, cudaMemcpyDeviceToHost, st);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+    if (qs != REMOE_OK || ce != cudaSuccess || !graph) {
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      if (qs != REMOE_OK) return qs;
+      return fail(REMOE_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+    }
+    g.graph = graph;
+    size_t n = 0;
+    CUDA_TRY(cudaGraphGetNodes(graph, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CUDA_TRY(cudaGraphGetNodes(graph, nodes.data(), &n));
+    for (cudaGraphNode_t nd : nodes) {
+      cudaGraphNodeType ty;
+      if (cudaGraphNodeGetType(nd, &ty) != cudaSuccess || ty != cudaGraphNodeTypeMemcpy) continue;
+      cudaMemcpy3DParms mp{};
+      if (cudaGraphMemcpyNodeGetParams(nd, &mp) != cudaSuccess) continue;
+      if (mp.dstPtr.ptr == h->hq) g.h2d = nd;
+      else if (mp.srcPtr.ptr == h->hids) g.d2h_ids = nd;
+      else if (mp.srcPtr.ptr == h->hscores) g.d2h_sc = nd;
+      else if (mp.srcPtr.ptr == h->hpred) g.d2h_pred = nd;
+    }
+    if (!g.h2d || !g.d2h_ids || !g.d2h_sc || (pred && !g.d2h_pred)) {
+      g.reset();
+      return fail(REMOE_ERR_CUDA, "graph capture: copy nodes not found");
+    }
+    CUDA_TRY(cudaGraphInstantiate(&g.exec, graph, 0));
+    g.B = B; g.k = k; g.pred = pred != nullptr; g.launches = launches;
+  }
+  CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(g.exec, g.h2d, h->hq, q, qb, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(g.exec, g.d2h_ids, ids, h->hids, ib, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(g.exec, g.d2h_sc, scores, h->hscores, sb, cudaMemcpyDeviceToHost));
+  if (pred)
+    CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(g.exec, g.d2h_pred, pred, h->hpred, pb, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaGraphLaunch(g.exec, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  h->last_launches = g.launches;
+  return REMOE_OK;
+}
+
 remoe_status_t remoe_sps_query_host(remoe_sps_t h, const uint16_t* q, int32_t B, int32_t k,
                                     int64_t* ids, float* scores, float* pred, void* stream) {
   ST_TRY(check_query(h, q, B, k, ids, scores));
@@ -581,6 +680,10 @@ remoe_status_t remoe_sps_query_host(remoe_sps_t h, const uint16_t* q, int32_t B,
   const int mb = h->cfg.max_batch;
   const int D = h->cfg.dim;
   int launches = 0;
+  if (B <= mb && h->cfg.world == 1 && !h->prof && !getenv("REMOE_NO_GRAPH")) {
+    remoe_status_t gs = query_host_graph(h, q, B, k, ids, scores, pred, st);
+    if (gs != REMOE_ERR_UNSUPPORTED) return gs;  // UNSUPPORTED: pageable buffers -> direct path
+  }
   for (int b0 = 0; b0 < B; b0 += mb) {
     const int bc = std::min(mb, B - b0);
     CUDA_TRY(cudaMemcpyAsync(h->hq, q + (size_t)b0 * D, (size_t)bc * D * 2, cudaMemcpyHostToDevice, st));
@@ -748,6 +851,10 @@ remoe_status_t remoe_sps_set_kernel(remoe_sps_t h, int32_t which) {
   if (which >= 2 && !h->tc.ok) return fail(REMOE_ERR_UNSUPPORTED, "tensor-core scan unavailable: %s", h->tc.why);
   if (which == 3 && !remoe::tc_pair_usable(&h->tc))
     return fail(REMOE_ERR_UNSUPPORTED, "CTA-pair tensor-core scan unavailable for this store");
+  if (h->force_kernel != which) {
+    DeviceGuard dg(h->cfg.device);
+    h->hg.reset();  // the cached host-query graph baked in the previous kernel choice
+  }
   h->force_kernel = which;
   return REMOE_OK;
 }

@@ -261,6 +261,29 @@ def test_host_path_matches_device_path():
         assert np.array_equal(u, v)
 
 
+def test_host_graph_path_matches_device_path():
+    """Pinned host buffers take the cached CUDA-graph replay of remoe_sps_query_host: every
+    call re-points the graph's copies at the caller's buffers (two buffer sets, a new
+    batch shape, pred on/off, a kernel switch), results bit-identical to the device path."""
+    c, x, a = store("c2", 20_000)
+    s = make(x, a, max_batch=16, max_k=16)
+    L, E = c.layers, c.experts
+    for B, k, want_pred, kern in ((12, 10, True, 0), (12, 10, True, 0), (5, 3, True, 0), (5, 3, False, 0),
+                                  (12, 10, True, 2), (12, 10, True, 0)):
+        q = gen.queries(c.store_seed, c.query_seed + B + k, 20_000, c.dim, B, mode=1)
+        s.set_kernel(kern)
+        d = run(s, q, k)
+        qh = torch.from_numpy(q.view(np.int16)).pin_memory()
+        ids = torch.full((B, k), -7, dtype=torch.int64).pin_memory()
+        sc = torch.full((B, k), -7.0, dtype=torch.float32).pin_memory()
+        pr = torch.full((B, L, E), -7.0, dtype=torch.float32).pin_memory() if want_pred else None
+        remoe.remoe_sps_query_host(s.handle, qh, B, k, ids, sc, pr)
+        assert np.array_equal(ids.numpy(), d[0]) and np.array_equal(sc.numpy(), d[1])
+        if want_pred:
+            assert np.array_equal(pr.numpy(), d[2])
+    s.set_kernel(0)
+
+
 # ------------------------------------------------------------------ S8 expert plan
 
 def test_expert_plan_vs_oracle():
