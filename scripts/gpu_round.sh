@@ -1,7 +1,7 @@
 #!/bin/bash
 # One GPU call: full gpu tests, smoke, and the default-config evidence.
-mkdir -p gpurun_out/r1s3
-nvidia-smi > gpurun_out/r1s3/smi.txt 2>&1
-timeout 1500 python -m pytest tests -m gpu -q -x --timeout 900 > gpurun_out/r1s3/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r1s3/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r1s3/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/r1s3/smoke.log
-timeout 900 bash scripts/round_profile.sh r1s3/c3_b64
+mkdir -p gpurun_out/r1s4
+nvidia-smi > gpurun_out/r1s4/smi.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -x --timeout 900 > gpurun_out/r1s4/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r1s4/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r1s4/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/r1s4/smoke.log
+timeout 900 bash scripts/round_profile.sh r1s4/c3_b64
