@@ -218,12 +218,23 @@ struct LaneTopk {
   __device__ __forceinline__ void push_ool(uint64_t key, int k) { load(push_call(save(), key, k, buf, g)); }
 
   // Whole warp: write each lane's sorted best k to out_of(lane) (k keys, zero padded).
+  // The sort network is sized to the lane's fill, not to CAP: with seeded thresholds a
+  // buffer usually holds a handful of keys, and sorting all CAP = 512 slots of 32 lanes
+  // one after another cost ~0.5 ms per scan at k = 128.
   __device__ __forceinline__ void flush(uint64_t* my_out, int k) {
+    const int lane = threadIdx.x & 31;
     for (int L = 0; L < 32; ++L) {
       uint64_t* b = (uint64_t*)__shfl_sync(kFull, (unsigned long long)buf, L);
       uint64_t* o = (uint64_t*)__shfl_sync(kFull, (unsigned long long)my_out, L);
       const int c = __shfl_sync(kFull, cnt, L);
-      if (o != nullptr) warp_compact<P>(b, c, k, o);
+      if (o == nullptr) continue;
+      int n;  // slots the network sorts and writes (those past c read as 0)
+      if (c <= 64 || P <= 2) { warp_compact<2>(b, c, k, o); n = 64; }
+      else if (c <= 128 || P <= 4) { warp_compact<(P < 4 ? P : 4)>(b, c, k, o); n = 128; }
+      else if (c <= 256 || P <= 8) { warp_compact<(P < 8 ? P : 8)>(b, c, k, o); n = 256; }
+      else { warp_compact<P>(b, c, k, o); n = CAP; }
+      for (int i = n + lane; i < k; i += 32) o[i] = 0ull;
+      __syncwarp();
     }
   }
 };

@@ -57,6 +57,7 @@ __device__ __forceinline__ void finalize_query(const uint64_t* tb, int k, int b,
 //      radix select finds the k-th largest key T exactly, and keys >= T are re-collected.
 constexpr int kSelCap = 2048;
 constexpr int kRankMax = 512;
+constexpr int kItemCap = 4096;
 
 __device__ __forceinline__ void block_sort_desc(uint64_t* a, int np2) {
   for (int size = 2; size <= np2; size <<= 1) {
@@ -84,6 +85,8 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
   __shared__ int cnt;
   __shared__ uint64_t prefix_s;
   __shared__ int need_s;
+  __shared__ uint32_t items_s[kItemCap];  // (list << 3) | chunk
+  __shared__ int n_items_s;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int b = blockIdx.x;
   pdl_wait();  // the scan's lists and thresholds
@@ -106,22 +109,54 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
     const int64_t l = f / list_len, i = f - l * list_len;
     return __ldg(base + l * lstride + i);
   };
+  auto append = [&](uint64_t key, uint64_t thr_lo) {  // whole warp; keys >= thr_lo to cand
+    const unsigned m = __ballot_sync(kFull, key >= thr_lo);
+    if (m) {
+      int pos0 = 0;
+      if (lane == 0) pos0 = atomicAdd(&cnt, __popc(m));
+      pos0 = __shfl_sync(kFull, pos0, 0);
+      const int pos = pos0 + __popc(m & ((1u << lane) - 1u));
+      if (key >= thr_lo && pos < kSelCap) cand[pos] = key;
+    }
+  };
   auto collect = [&](uint64_t thr_lo) {  // append keys >= thr_lo to cand (warp-aggregated)
     for (int64_t f0 = (int64_t)warp * 32 + lane; f0 - lane < n_keys; f0 += 8 * 256) {
       uint64_t kk[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) kk[u] = flat_key(f0 + 256 * u);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const unsigned m = __ballot_sync(kFull, kk[u] >= thr_lo);
-        if (m) {
-          int pos0 = 0;
-          if (lane == 0) pos0 = atomicAdd(&cnt, __popc(m));
-          pos0 = __shfl_sync(kFull, pos0, 0);
-          const int pos = pos0 + __popc(m & ((1u << lane) - 1u));
-          if (kk[u] >= thr_lo && pos < kSelCap) cand[pos] = kk[u];
+      for (int u = 0; u < 8; ++u) append(kk[u], thr_lo);
+    }
+  };
+  // Lists are sorted descending: chunk c + 1 of a list (32 keys) can hold a key >= thr_lo
+  // only if the last key of chunk c does.  With seeded thresholds most lists of a large
+  // k end after their first chunk, so only the needed (list, chunk) items are read.
+  auto collect_lists = [&](uint64_t thr_lo) {
+    if (t == 0) n_items_s = 0;
+    __syncthreads();
+    for (int l = t; l < n_lists; l += blockDim.x) {
+      const uint64_t* lp = base + (int64_t)l * lstride;
+      int need = 1;
+      while (need < nch && __ldg(lp + 32 * need - 1) >= thr_lo) ++need;
+      const int pos = atomicAdd(&n_items_s, need);
+      for (int c = 0; c < need; ++c) items_s[pos + c] = ((uint32_t)l << 3) | (uint32_t)c;
+    }
+    __syncthreads();
+    const int ni = n_items_s;
+    for (int i0 = warp; i0 < ni; i0 += 8 * 4) {
+      uint64_t kk[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int it = i0 + 8 * u;
+        kk[u] = 0ull;
+        if (it < ni) {
+          const uint32_t w = items_s[it];
+          const int i = (int)(w & 7u) * 32 + lane;
+          if (i < list_len) kk[u] = __ldg(base + (int64_t)(w >> 3) * lstride + i);
         }
       }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) append(kk[u], thr_lo);
     }
   };
   // Lists are sorted: the k-th largest list head is a real key <= the final k-th key,
@@ -143,7 +178,8 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
   }
   if (t == 0) cnt = 0;
   __syncthreads();
-  collect(lb);
+  if (nch >= 2 && nch <= 8 && (int64_t)n_lists * nch <= kItemCap) collect_lists(lb);
+  else collect(lb);
   __syncthreads();
   int n = cnt;
   if (n > kSelCap) {
