@@ -223,7 +223,21 @@ struct LaneTopk {
   // one after another cost ~0.5 ms per scan at k = 128.
   __device__ __forceinline__ void flush(uint64_t* my_out, int k) {
     const int lane = threadIdx.x & 31;
+    // lanes holding at most 32 keys sort their own buffer (insertion sort, all lanes at
+    // once) and write their list themselves; only fuller buffers take the warp network
+    const bool self = my_out != nullptr && cnt <= 32;
+    if (self) {
+      for (int i = 1; i < cnt; ++i) {
+        const uint64_t x = buf[i];
+        int j = i - 1;
+        while (j >= 0 && buf[j] < x) { buf[j + 1] = buf[j]; --j; }
+        buf[j + 1] = x;
+      }
+      for (int i = 0; i < k; ++i) my_out[i] = i < cnt ? buf[i] : 0ull;
+    }
+    const unsigned rest = __ballot_sync(kFull, my_out != nullptr && !self);
     for (int L = 0; L < 32; ++L) {
+      if (!((rest >> L) & 1u)) continue;
       uint64_t* b = (uint64_t*)__shfl_sync(kFull, (unsigned long long)buf, L);
       uint64_t* o = (uint64_t*)__shfl_sync(kFull, (unsigned long long)my_out, L);
       const int c = __shfl_sync(kFull, cnt, L);
@@ -401,9 +415,12 @@ __device__ __forceinline__ uint4 ldg_nc128(const void* p) {
   return r;
 }
 
-// CAP selection shared by host and device: CAP = 32*P >= max(64, pow2ceil(4k)).
+// CAP selection shared by host and device: CAP = 32*P >= max(64, pow2ceil(2k)), which
+// keeps CAP - k >= 32 (room for a chunk after a compaction) for every k <= 256.  (CAP =
+// pow2ceil(4k) made the k > 64 scans spill: the P = 16 sort network needs more registers
+// than the epilogue has, and seeded thresholds leave the buffers nearly empty anyway.)
 __host__ __device__ constexpr int topk_P(int k) {
-  return (4 * k <= 64) ? 2 : (4 * k <= 128) ? 4 : (4 * k <= 256) ? 8 : (4 * k <= 512) ? 16 : 32;
+  return (2 * k <= 64) ? 2 : (2 * k <= 128) ? 4 : (2 * k <= 256) ? 8 : (2 * k <= 512) ? 16 : 32;
 }
 
 }  // namespace remoe
