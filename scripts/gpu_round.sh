@@ -1,7 +1,9 @@
 #!/bin/bash
 # One GPU call: full gpu tests, smoke, and the default-config evidence.
-mkdir -p gpurun_out/r1s4
-nvidia-smi > gpurun_out/r1s4/smi.txt 2>&1
-timeout 1500 python -m pytest tests -m gpu -q -x --timeout 900 > gpurun_out/r1s4/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r1s4/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r1s4/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/r1s4/smoke.log
-timeout 900 bash scripts/round_profile.sh r1s4/c3_b64
+mkdir -p gpurun_out/r1s5
+nvidia-smi > gpurun_out/r1s5/smi.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -x --timeout 900 > gpurun_out/r1s5/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/r1s5/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r1s5/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/r1s5/smoke.log
+timeout 900 bash scripts/round_profile.sh r1s5/c3_b64
+timeout 600 bash scripts/round_profile.sh r1s5/c3_b64_k128 --config c3 --batch 64 --k 128
+timeout 600 bash scripts/round_profile.sh r1s5/c2_b16 --config c2 --batch 16
