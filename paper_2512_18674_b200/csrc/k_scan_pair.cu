@@ -56,7 +56,7 @@ struct PairArgs {
   const float* xnorm;
   int64_t n_rows;
   int64_t gid_offset;
-  const int64_t* gid_map;  // global id of row r = gid_map[r] if non-null, else gid_offset + r
+  int64_t gid_stride;      // global id of row r = gid_offset + r * gid_stride (seed samples: stride)
   int dim;
   const float* qnorm;      // [nq] of this launch
   int nq;                  // queries of this launch; group y, CTA rank r: [256 y + 128 r, +128)
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         }
         const int left = nvalid - c * 32;
         if (left < 32) mask &= left > 0 ? ((1u << left) - 1u) : 0u;
-        const int64_t gbase = p.gid_offset + row0 + c * 32;
+        const int64_t gbase = p.gid_offset + (row0 + c * 32) * p.gid_stride;
         if constexpr (KR > 0) {
           if (__any_sync(kFull, mask != 0)) {
             float vl[32];
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
               mask &= mask - 1;
               const float den = __fmaf_rn(qn, xc[j], p.sigma);
               if (vl[j] >= tk.tlim * den) {
-                const int64_t gid = p.gid_map ? p.gid_map[row0 + c * 32 + j] : gbase + j;
+                const int64_t gid = gbase + j * p.gid_stride;
                 tk.insert(make_key(__fdiv_rn(vl[j], den), gid));
               }
             }
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 const int j = 4 * j4 + u;
                 if ((mask >> j) & 1u) {
                   const float den = __fmaf_rn(qn, xx[u], p.sigma);
-                  const int64_t gid = p.gid_map ? p.gid_map[row0 + c * 32 + j] : gbase + j;
+                  const int64_t gid = gbase + j * p.gid_stride;
                   tk.append(make_key(__fdiv_rn(__uint_as_float(v[j]), den), gid));
                 }
               }
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 const int j = __ffs(mask) - 1;
                 mask &= mask - 1;
                 const float den = __fmaf_rn(qn, xc[j], p.sigma);
-                const int64_t gid = p.gid_map ? p.gid_map[row0 + c * 32 + j] : gbase + j;
+                const int64_t gid = gbase + j * p.gid_stride;
                 key = make_key(__fdiv_rn(vl[j], den), gid);
               }
               tk.push(key, p.k);
@@ -429,7 +429,7 @@ static cudaError_t launch_pair(const TcPlan* t, const CUtensorMap& tq, const Pai
 bool tc_pair_usable(const TcPlan* t) { return t->ok && t->grid >= 2 && encode_fn() != nullptr; }
 
 remoe_status_t tc_pair_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc, int k, float sigma,
-                            const float* xnorm, int64_t n_rows, int64_t gid_offset, const int64_t* gid_map,
+                            const float* xnorm, int64_t n_rows, int64_t gid_offset, int64_t gid_stride,
                             uint64_t* cand_buf, unsigned long long* gthr, uint64_t* lists, cudaStream_t st,
                             int* launches, int* lists_per_query) {
   if (!tc_pair_usable(t)) return REMOE_ERR_UNSUPPORTED;
@@ -476,7 +476,7 @@ remoe_status_t tc_pair_scan(TcPlan* t, const uint16_t* q, const float* qnorm, in
     a.xnorm = xnorm;
     a.n_rows = n_rows;
     a.gid_offset = gid_offset;
-    a.gid_map = gid_map;
+    a.gid_stride = gid_stride;
     a.dim = D;
     a.qnorm = qnorm + s0;
     a.nq = nq;

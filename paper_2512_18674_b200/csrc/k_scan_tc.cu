@@ -62,7 +62,7 @@ struct TcArgs {
   unsigned long long* gthr;  // [nq] shared thresholds (zeroed before the launch)
   uint64_t* out;
   int smem_bufs;  // candidate buffers in shared memory (else cand_buf in global memory)
-  const int64_t* gid_map;  // global id of row r = gid_map[r] if non-null, else gid_offset + r
+  int64_t gid_stride;      // global id of row r = gid_offset + r * gid_stride (seed samples: stride)
   int merge_in_cta;        // register top-k: merge the two parity states into one list per CTA
   int cluster;             // CTAs per cluster along y (multicast of the store tiles), 1 = none
   int epi_sleep;           // epilogue waits with a suspend-time hint (REMOE_EPI_SLEEP=1)
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             float vl[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) vl[j] = __uint_as_float(v[j]);
-            const int64_t gbase = p.gid_offset + row0 + c * 32;
+            const int64_t gbase = p.gid_offset + (row0 + c * 32) * p.gid_stride;
             if (p.stats) {
               atomicAdd(p.stats + 0, (unsigned long long)__popc(mask));
               if (lane == 0) atomicAdd(p.stats + 2, 1ull);
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               mask &= mask - 1;
               const float den = __fmaf_rn(qn, xc[j], p.sigma);
               if (vl[j] >= tk.tlim * den) {
-                const int64_t gid = p.gid_map ? p.gid_map[row0 + c * 32 + j] : gbase + j;
+                const int64_t gid = gbase + j * p.gid_stride;
                 const uint64_t key = make_key(__fdiv_rn(vl[j], den), gid);
                 if (p.stats && key > tk.thr) atomicAdd(p.stats + 1, 1ull);
                 tk.insert(key);
@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // many candidates (the first tiles, before the thresholds settle): compute all
             // keys of the chunk at once and append them (room for 32 guaranteed first)
             tk.ensure_room(32, p.k);
-            const int64_t gbase = p.gid_offset + row0 + c * 32;
+            const int64_t gbase = p.gid_offset + (row0 + c * 32) * p.gid_stride;
 #pragma unroll
             for (int j4 = 0; j4 < 8; ++j4) {
               const float4 x4 = lds128f(xc + 4 * j4);
@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int j = 4 * j4 + u;
                 if ((mask >> j) & 1u) {
                   const float den = __fmaf_rn(qn, xx[u], p.sigma);
-                  const int64_t gid = p.gid_map ? p.gid_map[row0 + c * 32 + j] : gbase + j;
+                  const int64_t gid = gbase + j * p.gid_stride;
                   tk.append(make_key(__fdiv_rn(__uint_as_float(v[j]), den), gid));
                 }
               }
@@ -417,14 +417,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             float vl[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) vl[j] = __uint_as_float(v[j]);
-            const int64_t gbase = p.gid_offset + row0 + c * 32;
+            const int64_t gbase = p.gid_offset + (row0 + c * 32) * p.gid_stride;
             while (__any_sync(kFull, mask != 0)) {
               uint64_t key = 0;
               if (mask) {
                 const int j = __ffs(mask) - 1;
                 mask &= mask - 1;
                 const float den = __fmaf_rn(qn, xc[j], p.sigma);
-                const int64_t gid = p.gid_map ? p.gid_map[row0 + c * 32 + j] : gbase + j;
+                const int64_t gid = gbase + j * p.gid_stride;
                 key = make_key(__fdiv_rn(vl[j], den), gid);
               }
               tk.push(key, p.k);
@@ -633,7 +633,7 @@ static cudaError_t launch_tc_m(const TcPlan* t, const TcArgs& a, dim3 g, cudaStr
 }
 
 remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc, int k, float sigma,
-                       const float* xnorm, int64_t n_rows, int64_t gid_offset, const int64_t* gid_map,
+                       const float* xnorm, int64_t n_rows, int64_t gid_offset, int64_t gid_stride,
                        uint64_t* cand_buf, unsigned long long* gthr, uint64_t* lists, cudaStream_t st,
                        int* launches, int* lists_per_query) {
   if (!t->ok) return REMOE_ERR_UNSUPPORTED;
@@ -673,7 +673,7 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
     a.n_stages = nst;
     a.cand_buf = cand_buf;
     a.gthr = gthr + s0;
-    a.gid_map = gid_map;
+    a.gid_stride = gid_stride;
     a.out = lists + (size_t)s0 * ctas_per_slab * lists_per_cta * k;
     a.merge_in_cta = in_cta ? 1 : 0;
     a.smem_bufs = smem_bufs ? 1 : 0;

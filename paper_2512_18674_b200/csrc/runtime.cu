@@ -115,7 +115,6 @@ struct remoe_sps {
     int64_t stride = 0, rows = 0;  // rows j * stride, j < rows
     remoe::TcPlan tc{};            // strided tensor map over the store
     float* xns = nullptr;          // their norms
-    int64_t* gids = nullptr;       // their global ids
   };
   SeedSample seeds[4];  // strides 64, 32, 16, 8 (larger k takes a denser sample)
   int n_seeds = 0;
@@ -370,11 +369,7 @@ static remoe_status_t build_impl(remoe_sps* h, const uint16_t* emb, const float*
       sd.stride = stride;
       sd.rows = S;
       ST_TRY(h->alloc((void**)&sd.xns, (size_t)S * 4));
-      ST_TRY(h->alloc((void**)&sd.gids, (size_t)S * 8));
       CUDA_TRY(cudaMemcpy2DAsync(sd.xns, 4, h->xnorm, (size_t)stride * 4, 4, S, cudaMemcpyDeviceToDevice, st));
-      std::vector<int64_t> g(S);
-      for (int64_t j = 0; j < S; ++j) g[j] = c.global_offset + j * stride;
-      CUDA_TRY(cudaMemcpyAsync(sd.gids, g.data(), S * 8, cudaMemcpyHostToDevice, st));
       CUDA_TRY(cudaStreamSynchronize(st));
       ST_TRY(remoe::tc_plan_create(&sd.tc, h->x, S, c.dim, h->num_sms, c.max_k, stride * c.dim));
       if (sd.tc.ok) ++h->n_seeds;
@@ -525,10 +520,10 @@ static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k
       int sl = 0;
       const remoe_status_t ss =
           which == 3 ? remoe::tc_pair_scan(const_cast<remoe::TcPlan*>(&sd->tc), q, h->qnorm, bc, ks, c.sigma, sd->xns,
-                                           sd->rows, 0, sd->gids, h->cand_buf, h->gthr + c.max_batch, h->lists, st,
+                                           sd->rows, c.global_offset, sd->stride, h->cand_buf, h->gthr + c.max_batch, h->lists, st,
                                            &nl, &sl)
                      : remoe::tc_scan(const_cast<remoe::TcPlan*>(&sd->tc), q, h->qnorm, bc, ks, c.sigma, sd->xns,
-                                      sd->rows, 0, sd->gids, h->cand_buf, h->gthr + c.max_batch, h->lists, st, &nl,
+                                      sd->rows, c.global_offset, sd->stride, h->cand_buf, h->gthr + c.max_batch, h->lists, st, &nl,
                                       &sl);
       if (ss != REMOE_OK)
         return fail(ss, "seed scan launch failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -539,9 +534,9 @@ static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k
     }
     const remoe_status_t ts =
         which == 3 ? remoe::tc_pair_scan(&h->tc, q, h->qnorm, bc, k, c.sigma, h->xnorm, c.n_local, c.global_offset,
-                                         nullptr, h->cand_buf, h->gthr, h->lists, st, &nl, &grid)
+                                         1, h->cand_buf, h->gthr, h->lists, st, &nl, &grid)
                    : remoe::tc_scan(&h->tc, q, h->qnorm, bc, k, c.sigma, h->xnorm, c.n_local, c.global_offset,
-                                    nullptr, h->cand_buf, h->gthr, h->lists, st, &nl, &grid);
+                                    1, h->cand_buf, h->gthr, h->lists, st, &nl, &grid);
     if (ts != REMOE_OK)
       return fail(ts, "tensor-core scan launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     *launches += nl;

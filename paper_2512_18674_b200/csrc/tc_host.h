@@ -66,16 +66,17 @@ void tc_plan_destroy(TcPlan* t);
 // Scores bc queries (any bc >= 1; 64 or 128 queries per pass) and writes sorted
 // top-k key lists: *lists_per_query lists of k keys per query,
 // lists[(b * lists_per_query + l) * k + i].
-// gid_map (optional): global id of row r is gid_map[r] instead of gid_offset + r.
+// gid_stride: global id of row r is gid_offset + r * gid_stride (1 for a shard, the
+// sample stride for the seeding sample: an arithmetic id, no per-candidate id load).
 remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc, int k, float sigma,
-                       const float* xnorm, int64_t n_rows, int64_t gid_offset, const int64_t* gid_map,
+                       const float* xnorm, int64_t n_rows, int64_t gid_offset, int64_t gid_stride,
                        uint64_t* cand_buf, unsigned long long* gthr, uint64_t* lists, cudaStream_t st,
                        int* launches, int* lists_per_query);
 // Large batches: the CTA-pair (cta_group::2) GEMM-tiled scan (k_scan_pair.cu), same
 // output contract as tc_scan; 256 queries per pair.
 bool tc_pair_usable(const TcPlan* t);
 remoe_status_t tc_pair_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc, int k, float sigma,
-                            const float* xnorm, int64_t n_rows, int64_t gid_offset, const int64_t* gid_map,
+                            const float* xnorm, int64_t n_rows, int64_t gid_offset, int64_t gid_stride,
                             uint64_t* cand_buf, unsigned long long* gthr, uint64_t* lists, cudaStream_t st,
                             int* launches, int* lists_per_query);
 // Batches of at least this many queries use the pair scan (REMOE_PAIR_MIN_B overrides).
