@@ -41,6 +41,23 @@ __device__ __forceinline__ float eq11(float dot, float qn, float xn, float sigma
   return __fdiv_rn(dot, __fmaf_rn(qn, xn, sigma));
 }
 
+// v[j] for a run-time j in [0, 32) as a 5-level select tree over registers.  Indexing a
+// register array with a run-time j makes nvcc copy the whole array to the local stack
+// (ncu: ~57 MB of local-store write-back to DRAM per 1M-row scan launch); 31 SELs per
+// candidate keep it in registers.
+__device__ __forceinline__ uint32_t sel32(const uint32_t (&v)[32], int j) {
+  uint32_t a[16], b[8], c[4], d[2];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = (j & 16) ? v[i + 16] : v[i];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) b[i] = (j & 8) ? a[i + 8] : a[i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i] = (j & 4) ? b[i + 4] : b[i];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) d[i] = (j & 2) ? c[i + 2] : c[i];
+  return (j & 1) ? d[1] : d[0];
+}
+
 // bf16 bit pairs packed in a 32-bit word -> fp32 (exact)
 __device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }

@@ -264,16 +264,14 @@ __global__ void __launch_bounds__(kPThreads, 1)
         const int64_t gbase = p.gid_offset + (row0 + c * 32) * p.gid_stride;
         if constexpr (KR > 0) {
           if (__any_sync(kFull, mask != 0)) {
-            float vl[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) vl[j] = __uint_as_float(v[j]);
             while (mask) {  // per lane: insertion network, no warp synchronisation
               const int j = __ffs(mask) - 1;
               mask &= mask - 1;
               const float den = __fmaf_rn(qn, xc[j], p.sigma);
-              if (vl[j] >= tk.tlim * den) {
+              const float vj = __uint_as_float(sel32(v, j));
+              if (vj >= tk.tlim * den) {
                 const int64_t gid = gbase + j * p.gid_stride;
-                tk.insert(make_key(__fdiv_rn(vl[j], den), gid));
+                tk.insert(make_key(__fdiv_rn(vj, den), gid));
               }
             }
             if (active && tk.thr > pair_pub) {
@@ -300,9 +298,6 @@ __global__ void __launch_bounds__(kPThreads, 1)
               }
             }
           } else if (__any_sync(kFull, mask != 0)) {
-            float vl[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) vl[j] = __uint_as_float(v[j]);
             while (__any_sync(kFull, mask != 0)) {
               uint64_t key = 0;
               if (mask) {
@@ -310,7 +305,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                 mask &= mask - 1;
                 const float den = __fmaf_rn(qn, xc[j], p.sigma);
                 const int64_t gid = gbase + j * p.gid_stride;
-                key = make_key(__fdiv_rn(vl[j], den), gid);
+                key = make_key(__fdiv_rn(__uint_as_float(sel32(v, j)), den), gid);
               }
               tk.push(key, p.k);
             }

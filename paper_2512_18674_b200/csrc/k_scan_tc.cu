@@ -368,9 +368,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (left < 32) mask &= left > 0 ? ((1u << left) - 1u) : 0u;
         if constexpr (KR > 0) {
           if (__any_sync(kFull, mask != 0)) {
-            float vl[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) vl[j] = __uint_as_float(v[j]);
             const int64_t gbase = p.gid_offset + (row0 + c * 32) * p.gid_stride;
             if (p.stats) {
               atomicAdd(p.stats + 0, (unsigned long long)__popc(mask));
@@ -380,9 +377,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int j = __ffs(mask) - 1;
               mask &= mask - 1;
               const float den = __fmaf_rn(qn, xc[j], p.sigma);
-              if (vl[j] >= tk.tlim * den) {
+              const float vj = __uint_as_float(sel32(v, j));
+              if (vj >= tk.tlim * den) {
                 const int64_t gid = gbase + j * p.gid_stride;
-                const uint64_t key = make_key(__fdiv_rn(vl[j], den), gid);
+                const uint64_t key = make_key(__fdiv_rn(vj, den), gid);
                 if (p.stats && key > tk.thr) atomicAdd(p.stats + 1, 1ull);
                 tk.insert(key);
               }
@@ -414,9 +412,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           } else if (__any_sync(kFull, mask != 0)) {
-            float vl[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) vl[j] = __uint_as_float(v[j]);
             const int64_t gbase = p.gid_offset + (row0 + c * 32) * p.gid_stride;
             while (__any_sync(kFull, mask != 0)) {
               uint64_t key = 0;
@@ -425,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mask &= mask - 1;
                 const float den = __fmaf_rn(qn, xc[j], p.sigma);
                 const int64_t gid = gbase + j * p.gid_stride;
-                key = make_key(__fdiv_rn(vl[j], den), gid);
+                key = make_key(__fdiv_rn(__uint_as_float(sel32(v, j)), den), gid);
               }
               tk.push(key, p.k);
             }
