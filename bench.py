@@ -231,9 +231,10 @@ def run_ours(args):
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush_buf = torch.empty(2 * l2 // 4 + 1024, dtype=torch.int32, device=dev)
     # the write pass leaves L2 full of dirty lines whose write-back would otherwise land
-    # inside the next step (~50 MB of DRAM writes in the scan, per ncu); a read pass over a
-    # second 2xL2 buffer evicts them before the step starts, so every step begins with a
-    # clean, cold L2 (as after a previous read-only query)
+    # inside the next step; a read pass over a second 2xL2 buffer evicts them before the
+    # step starts, so every step begins with a clean, cold L2 (as after a previous
+    # read-only query).  (The ~50 MB of scan DRAM writes ncu showed were the scan's own
+    # local-memory stores, fixed by sel32 in common.cuh, not this.)
     flush_rd = torch.zeros(2 * l2 // 4 + 1024, dtype=torch.int32, device=dev)
     flush = not args.no_flush
 
