@@ -78,10 +78,10 @@ CONFIGS = {
 
 
 def shard_range(n_total: int, world: int, rank: int) -> tuple[int, int]:
-    """Contiguous row shard of rank: [offset, offset+n_local)."""
-    per = -(-n_total // world)
-    lo = min(n_total, rank * per)
-    hi = min(n_total, lo + per)
+    """Contiguous row shard of rank: [offset, offset+n_local), the
+    balanced split offset_g = floor(n_total * g / world): no shard is empty for n >= world."""
+    lo = n_total * rank // world
+    hi = n_total * (rank + 1) // world
     return lo, hi - lo
 
 

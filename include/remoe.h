@@ -68,6 +68,7 @@ typedef enum {
 } remoe_status_t;
 
 typedef struct remoe_sps* remoe_sps_t; /* opaque, library-owned */
+typedef struct remoe_group* remoe_group_t; /* opaque loopback group (see remoe_loopback_group_create) */
 
 /*
  * Build configuration.  One per rank; the store is sharded row-wise into
@@ -90,6 +91,10 @@ typedef struct {
   const void* nccl_unique_id; /* 128-byte ncclUniqueId identical on all ranks; NULL iff world == 1 */
   int32_t inputs_on_device;   /* 1: emb/act passed to build are device pointers on `device`; 0: host */
   int32_t validate;       /* 1: reject non-finite embeddings, act < 0, |row sum - 1| > 1e-3 */
+  const void* loopback_group; /* world > 1 without NCCL: the remoe_group_t this rank joins (all
+                                 ranks in this process, on one device; exchanges are device copies).
+                                 NULL otherwise.  Exactly one of nccl_unique_id / loopback_group
+                                 is non-NULL when world > 1. */
 } remoe_sps_config_t;
 
 /* Fill *cfg with defaults (sigma 1e-6, T 1, max_batch 256, max_k 128, world 1,
@@ -105,6 +110,12 @@ REMOE_API void remoe_sps_config_default(remoe_sps_config_t* cfg);
  *   out:      receives the handle on success, NULL on failure.
  * Collective over `world` ranks (all ranks must call it).  Synchronous: returns
  * after the device copies and the |x_j| pass have completed.
+ * Multi-rank builds agree on the outcome: once the NCCL communicator exists, every
+ * rank contributes (offset, n_local, local status) to one all-gather, and if any rank
+ * failed (bad shard, validation, OOM, ...) every rank returns an error (the failing
+ * rank its own; the others that rank's status), so no rank is left blocked in a later
+ * collective.  Shards must tile [0, N_total) in rank order and hold >= 1 row each
+ * (the balanced split offset_g = floor(N g / G) does for N >= G).
  */
 REMOE_API remoe_status_t remoe_sps_build(const remoe_sps_config_t* cfg, const uint16_t* emb_bf16,
                                          const float* act, remoe_sps_t* out);
@@ -125,6 +136,23 @@ REMOE_API remoe_status_t remoe_sps_build(const remoe_sps_config_t* cfg, const ui
 REMOE_API remoe_status_t remoe_sps_query(remoe_sps_t h, const uint16_t* q_bf16, int32_t B,
                                          int32_t k, int64_t* ids, float* scores, float* pred,
                                          void* stream);
+
+/*
+ * Alignment (checked synchronously, INVALID_ARG): q_bf16 and pred must be 16-byte
+ * aligned (16-byte vector loads / cp.async of the query rows, float4 stores of the
+ * prediction), ids 8 bytes, scores 4 bytes.
+ *
+ * Multi-rank data path (world > 1, "top-alpha" over all history):
+ * each rank scans its shard (S1-S4); its B x k local keys are all-gathered; every rank
+ * merges the G lists with the same deterministic merge (S5: identical ids and scores on
+ * every rank); each rank then reduces only the winners it OWNS into a partial
+ * P_g = sum over owned r of w_r S~_{id_r} ("reduction on the owning ranks",
+ * BASELINE north_star); the partials are exchanged (all-gather of [G][B][L*E] while that
+ * is <= 32 MiB, REMOE_XCHG_AG_MAX at build; otherwise an all-to-all of query slices plus
+ * a broadcast of the finished slices) and summed in rank order g = 0..G-1, so every rank
+ * and every batch position gets the same bits.  Versus world == 1 the ids and scores are
+ * bit-identical; pred differs only by fp32 re-association (<= ~1e-7).
+ */
 
 /*
  * Same as remoe_sps_query, but q/ids/scores/pred are HOST buffers (pinned or
@@ -219,6 +247,29 @@ REMOE_API remoe_status_t remoe_sps_tree_query(remoe_sps_t h, const uint16_t* q_b
                                               int64_t* ids, float* scores, float* pred, int32_t* leaf,
                                               int32_t* n_eval, void* stream);
 
+/*
+ * Loopback groups: the multi-rank path (S5 exchange + merge, the owner-side partial S7
+ * and its exchange) run inside ONE process on ONE device, for testing and for emulating
+ * a G-GPU partition on one GPU.  remoe_loopback_group_create makes an empty group of
+ * `world` ranks; each rank's handle is built with remoe_sps_build (cfg.world = world,
+ * cfg.rank, cfg.loopback_group = the group, nccl_unique_id = NULL); the exchanges are
+ * device-to-device copies of exactly the bytes the NCCL collectives would move.
+ * remoe_loopback_group_destroy returns REMOE_ERR_STATE while handles are still built.
+ */
+REMOE_API remoe_status_t remoe_loopback_group_create(int32_t world, remoe_group_t* out);
+REMOE_API remoe_status_t remoe_loopback_group_destroy(remoe_group_t g);
+
+/*
+ * remoe_sps_query for every rank of a loopback group at once: ids[r], scores[r], pred[r]
+ * are rank r's device output buffers (the same shapes as remoe_sps_query; pred NULL, or
+ * an array of `world` buffers).  Every rank's outputs are written; they are identical.
+ * REMOE_ERR_STATE if a rank is missing; INVALID_ARG if the shards do not tile [0, N).
+ * remoe_sps_query on a group member returns REMOE_ERR_STATE.
+ */
+REMOE_API remoe_status_t remoe_sps_query_group(remoe_group_t g, const uint16_t* q_bf16, int32_t B, int32_t k,
+                                               int64_t* const* ids, float* const* scores, float* const* pred,
+                                               void* stream);
+
 /* Rank 0 calls this, then broadcasts the 128 bytes to all ranks (e.g. as a uint8
  * tensor over a torch.distributed group) before remoe_sps_build. */
 REMOE_API remoe_status_t remoe_nccl_unique_id(uint8_t out[128]);
@@ -240,7 +291,8 @@ REMOE_API remoe_status_t remoe_sps_get_info(remoe_sps_t h, remoe_sps_info_t* inf
 
 /* Force the scan kernel: 0 auto (default), 1 streaming, 2 tensor core (resident query slab),
  * 3 tensor core on CTA pairs (the large-batch GEMM tiling).  Auto picks 3 for batches of
- * at least 256 queries (REMOE_PAIR_MIN_B overrides), else 2 when the store allows it.
+ * at least 128 queries (REMOE_PAIR_MIN_B overrides), else 2 when the store allows it
+ * (D % 64 == 0 and D <= 1536), else 1 (the only kernel for 1536 < D <= 4096).
  * Also settable with the environment variable REMOE_FORCE_KERNEL=stream|tc|pair.
  * INVALID_ARG for other values, UNSUPPORTED when the kernel cannot serve this store. */
 REMOE_API remoe_status_t remoe_sps_set_kernel(remoe_sps_t h, int32_t which);

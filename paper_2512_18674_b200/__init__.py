@@ -8,7 +8,8 @@ from .sps import (  # noqa: F401
     SpsInfo, lib, remoe_expert_plan, remoe_nccl_unique_id, remoe_sps_build,
     remoe_sps_config_default, remoe_sps_destroy, remoe_sps_get_info, remoe_sps_profile, remoe_sps_query,
     remoe_sps_query_host, remoe_sps_set_kernel, remoe_sps_sync, remoe_sps_embed, embed, remoe_js_divergence, js_divergence,
-    TreeInfo, remoe_sps_tree_build, remoe_sps_tree_info, remoe_sps_tree_export, remoe_sps_tree_query,
+    TreeInfo, remoe_sps_tree_build, LoopbackGroup, remoe_loopback_group_create,
+    remoe_loopback_group_destroy, remoe_sps_query_group, remoe_sps_tree_info, remoe_sps_tree_export, remoe_sps_tree_query,
 )
 from .planner import (  # noqa: F401
     PLANNER_FUNCTIONS, remoe_convexity_threshold, remoe_fit_latency_curve, remoe_greedy_replicas,

@@ -2,7 +2,9 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <set>
 #include <utility>
 
@@ -88,6 +90,25 @@ inline int max_active_clusters(const void* kern, dim3 block, size_t smem, unsign
     cudaGetLastError();
     return 0;
   }
+  return n;
+}
+
+// max_active_clusters, cached per (kernel, block, smem, cluster size, device): the occupancy
+// query is not free and the answer never changes for a given launch shape.
+inline int max_active_clusters_cached(const void* kern, dim3 block, size_t smem, unsigned cy) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, unsigned, size_t, unsigned, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(kern, block.x * block.y * block.z, smem, cy, dev);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  const int n = max_active_clusters(kern, block, smem, cy);
+  std::lock_guard<std::mutex> lock(mu);
+  cache[key] = n;
   return n;
 }
 

@@ -5,6 +5,8 @@
 #include "host_util.h"
 #include "kernels.h"
 
+#include <algorithm>
+
 namespace remoe {
 
 // ---------------------------------------------------------------- S0 / S1 norms
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
     const uint64_t kth = k <= nout ? topk[k - 1] : 0ull;
     set_thr[b] = kth ? kth - 1 : 0ull;
   }
-  if (fin.act != nullptr || fin.rows != nullptr) {  // fused S6 + S7 (world == 1)
+  if (fin.act != nullptr) {  // fused S6 + S7 (one GPU) or S6 + partial S7 (multi-GPU)
     if (nout < k)
       for (int i = nout + t; i < k; i += blockDim.x) topk[i] = 0ull;
     __syncthreads();
@@ -279,16 +281,19 @@ cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride
 // ---------------------------------------------------------------- S6 + S7
 // w_r = softmax(s_r / T), max-subtracted: s_0 is the largest score of the
 // sorted list.  exp in parallel, the normaliser by a fixed xor tree (order
-// independent of batch position).  P[e] = sum_r w_r A_r[e], r ascending.
+// independent of batch position).  P[e] = sum_r w_r A_r[e], r ascending over the rows
+// that contribute (all k on one GPU; the owned ones for a multi-GPU partial, mode 2).
 // Whole CTA (256 threads); outputs j = j0 + t, j0 + t + 256, ... < j1.
 __device__ __forceinline__ void finalize_query(const uint64_t* tb, int k, int b, const FinalizeArgs& f,
                                                int64_t j0, int64_t j1, bool write_ids) {
   __shared__ float w[256];
   __shared__ const float* src[256];
   __shared__ float red[8];
-  const int t = threadIdx.x;
+  __shared__ int wcnt[8];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const float s0 = key_score(tb[0]);
   float e = 0.f;
+  const float* my_src = nullptr;
   if (t < k) {
     const uint64_t key = tb[t];
     if (key != 0) {
@@ -299,25 +304,34 @@ __device__ __forceinline__ void finalize_query(const uint64_t* tb, int k, int b,
         f.scores[(int64_t)b * k + t] = s;
       }
       e = expf(__fdiv_rn(s - s0, f.T));
-      src[t] = f.mode == 0 ? f.act + (gid - f.offset) * f.LE : f.rows + ((int64_t)b * k + t) * f.LE;
-    } else {  // fewer than k candidates (cannot happen for k <= N_total): empty slot
-      if (write_ids) {
-        f.ids[(int64_t)b * k + t] = -1;
-        f.scores[(int64_t)b * k + t] = -__int_as_float(0x7f800000);
-      }
-      src[t] = f.mode == 0 ? f.act : f.rows;  // weight 0
+      const int64_t j = gid - f.offset;
+      if (j >= 0 && j < f.n_local) my_src = f.act + j * f.LE;  // a row this rank holds
+    } else if (write_ids) {  // fewer than k candidates (cannot happen for k <= N_total): empty slot
+      f.ids[(int64_t)b * k + t] = -1;
+      f.scores[(int64_t)b * k + t] = -__int_as_float(0x7f800000);
     }
   }
   if (f.pred == nullptr) return;
   float z = e;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(kFull, z, off);
-  if ((t & 31) == 0) red[t >> 5] = z;
+  // compaction of the contributing rows, r ascending (warp ballots + an 8-entry scan)
+  const unsigned keep = __ballot_sync(kFull, my_src != nullptr);
+  if (lane == 0) { red[warp] = z; wcnt[warp] = __popc(keep); }
   __syncthreads();
   float Z = 0.f;
+  int before = 0, nr = 0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) Z += red[i];
-  if (t < k) w[t] = __fdiv_rn(e, Z);
+  for (int i = 0; i < 8; ++i) {
+    Z += red[i];
+    before += i < warp ? wcnt[i] : 0;
+    nr += wcnt[i];
+  }
+  if (my_src != nullptr) {
+    const int pos = before + __popc(keep & ((1u << lane) - 1u));
+    w[pos] = __fdiv_rn(e, Z);
+    src[pos] = my_src;
+  }
   __syncthreads();
   if ((f.LE & 3) == 0 && (j0 & 3) == 0 && ((j1 & 3) == 0 || j1 == f.LE)) {
     // float4 columns, two per thread per step, 8 rows at a time (16 x 16-byte loads in
@@ -327,18 +341,18 @@ __device__ __forceinline__ void finalize_query(const uint64_t* tb, int k, int b,
       const int64_t cb = ca + blockDim.x;
       const bool vb = cb < c1;
       float4 acc_a = make_float4(0.f, 0.f, 0.f, 0.f), acc_b = acc_a;
-      for (int r0 = 0; r0 < k; r0 += 8) {
+      for (int r0 = 0; r0 < nr; r0 += 8) {
         float4 xa[8], xb[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const bool vr = r0 + u < k;
-          const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-          xa[u] = vr ? __ldg(reinterpret_cast<const float4*>(src[r0 + u]) + ca) : z;
-          xb[u] = (vr && vb) ? __ldg(reinterpret_cast<const float4*>(src[r0 + u]) + cb) : z;
+          const bool vr = r0 + u < nr;
+          const float4 zz = make_float4(0.f, 0.f, 0.f, 0.f);
+          xa[u] = vr ? __ldg(reinterpret_cast<const float4*>(src[r0 + u]) + ca) : zz;
+          xb[u] = (vr && vb) ? __ldg(reinterpret_cast<const float4*>(src[r0 + u]) + cb) : zz;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          if (r0 + u < k) {  // r ascending
+          if (r0 + u < nr) {  // r ascending
             const float wr = w[r0 + u];
             acc_a.x = __fmaf_rn(wr, xa[u].x, acc_a.x); acc_a.y = __fmaf_rn(wr, xa[u].y, acc_a.y);
             acc_a.z = __fmaf_rn(wr, xa[u].z, acc_a.z); acc_a.w = __fmaf_rn(wr, xa[u].w, acc_a.w);
@@ -357,17 +371,17 @@ __device__ __forceinline__ void finalize_query(const uint64_t* tb, int k, int b,
     const int64_t jb = ja + blockDim.x;
     const bool vb = jb < j1;
     float acc_a = 0.f, acc_b = 0.f;
-    for (int r0 = 0; r0 < k; r0 += 8) {
+    for (int r0 = 0; r0 < nr; r0 += 8) {
       float xa[8], xb[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const bool vr = r0 + u < k;
+        const bool vr = r0 + u < nr;
         xa[u] = vr ? __ldg(src[r0 + u] + ja) : 0.f;
         xb[u] = (vr && vb) ? __ldg(src[r0 + u] + jb) : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        if (r0 + u < k) {  // r ascending
+        if (r0 + u < nr) {  // r ascending
           acc_a = __fmaf_rn(w[r0 + u], xa[u], acc_a);
           acc_b = __fmaf_rn(w[r0 + u], xb[u], acc_b);
         }
@@ -383,40 +397,52 @@ __device__ __forceinline__ void finalize_query(const uint64_t* tb, int k, int b,
 __global__ void __launch_bounds__(256) k_finalize(const uint64_t* __restrict__ top, int k, FinalizeArgs f) {
   const int b = blockIdx.x;
   const int64_t j0 = (int64_t)blockIdx.y * blockDim.x;
+  pdl_wait();
   finalize_query(top + (int64_t)b * k, k, b, f, j0, j0 + blockDim.x < f.LE ? j0 + blockDim.x : f.LE,
                  blockIdx.y == 0);
 }
 
-cudaError_t launch_finalize(const uint64_t* top, int B, int k, const float* act, int64_t offset,
-                            const float* rows, int mode, int64_t LE, float temperature,
-                            int64_t* ids, float* scores, float* pred, cudaStream_t st) {
+cudaError_t launch_finalize(const uint64_t* top, int B, int k, const FinalizeArgs& f, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
   if (k > 256) return cudaErrorInvalidValue;
-  const FinalizeArgs f{act, offset, rows, mode, LE, temperature, ids, scores, pred};
-  const unsigned chunks = pred ? (unsigned)((LE + 255) / 256) : 1u;
+  const unsigned chunks = f.pred ? (unsigned)((f.LE + 255) / 256) : 1u;
   cudaError_t e = set_smem_attrs_once((const void*)k_finalize, 0);
   if (e != cudaSuccess) return e;
-  k_finalize<<<dim3((unsigned)B, chunks), 256, 0, st>>>(top, k, f);
-  return cudaGetLastError();
+  return launch_pdl(k_finalize, dim3((unsigned)B, chunks), dim3(256), 0, st, top, k, f);
 }
 
-// ---------------------------------------------------------------- multi-GPU row gather
-__global__ void k_gather_rows(const uint64_t* __restrict__ top, int k, const float* __restrict__ act,
-                              int64_t offset, int64_t n_local, int64_t LE, float* __restrict__ rows) {
-  const int64_t br = blockIdx.x;  // b * k + r
-  const int64_t gid = key_gid(top[br]);
-  const int64_t j = gid - offset;
-  const bool own = j >= 0 && j < n_local;
-  float* dst = rows + br * LE;
-  const float* s = act + (own ? j : 0) * LE;
-  for (int64_t e = threadIdx.x; e < LE; e += blockDim.x) dst[e] = own ? s[e] : 0.f;
+// ---------------------------------------------------------------- multi-GPU S7 combine
+// out[i] = parts[0][i] + parts[1][i] + ... + parts[G-1][i], g ascending: every rank sums
+// the same gathered partials in the same order, so all ranks (and every batch position)
+// get identical bits (ncclAllReduce's ring order would not guarantee that).
+__global__ void k_psum(const float* __restrict__ parts, int G, int64_t stride, int64_t n, float* __restrict__ out) {
+  pdl_wait();
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  if ((stride & 3) == 0 && (n & 3) == 0 && ((reinterpret_cast<uintptr_t>(parts) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n >> 2); i += step) {
+      float4 acc = __ldg(reinterpret_cast<const float4*>(parts) + i);
+      for (int g = 1; g < G; ++g) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(parts + g * stride) + i);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+      reinterpret_cast<float4*>(out)[i] = acc;
+    }
+    return;
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += step) {
+    float acc = parts[i];
+    for (int g = 1; g < G; ++g) acc += parts[g * stride + i];
+    out[i] = acc;
+  }
 }
 
-cudaError_t launch_gather_rows(const uint64_t* top, int B, int k, const float* act, int64_t offset,
-                               int64_t n_local, int64_t LE, float* rows, cudaStream_t st) {
-  if (B <= 0) return cudaSuccess;
-  k_gather_rows<<<(unsigned)((int64_t)B * k), 256, 0, st>>>(top, k, act, offset, n_local, LE, rows);
-  return cudaGetLastError();
+cudaError_t launch_psum(const float* parts, int G, int64_t part_stride, int64_t n, float* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t units = (n + 3) / 4;
+  const unsigned grid = (unsigned)std::min<int64_t>((units + 255) / 256, 148 * 8);
+  cudaError_t e = set_smem_attrs_once((const void*)k_psum, 0);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(k_psum, dim3(grid), dim3(256), 0, st, parts, G, part_stride, n, out);
 }
 
 // ---------------------------------------------------------------- S8 plan

@@ -463,11 +463,11 @@ remoe_status_t tc_pair_scan(TcPlan* t, const uint16_t* q, const float* qnorm, in
     const cuuint32_t box[2] = {(cuuint32_t)kPBK, 128u};
     const cuuint32_t estr[2] = {1, 1};
     if (enc(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(q + (size_t)s0 * D), gdim, gstride,
-            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, tmap_promotion(),
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, t->kn.promotion(),
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return REMOE_ERR_CUDA;
     PairArgs a{};
-    a.kb_order = kb_order_env();
+    a.kb_order = t->kn.kb_order;
     a.xnorm = xnorm;
     a.n_rows = n_rows;
     a.gid_offset = gid_offset;
@@ -483,7 +483,7 @@ remoe_status_t tc_pair_scan(TcPlan* t, const uint16_t* q, const float* qnorm, in
     a.out = lists + (size_t)s0 * (*lists_per_query) * k;
     a.smem_bufs = smem_bufs ? 1 : 0;
     a.merge_in_cta = in_cta ? 1 : 0;
-    if (getenv("REMOE_VERBOSE"))
+    if (t->kn.verbose)
       fprintf(stderr, "[remoe] pair scan grid (%d,%d) stages %d lists/query %d\n", 2 * ppg, ng, nst,
               *lists_per_query);
     if (launch_pair(t, tq, a, dim3((unsigned)(2 * ppg), (unsigned)ng), st) != cudaSuccess) return REMOE_ERR_CUDA;

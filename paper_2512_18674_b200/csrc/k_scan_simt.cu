@@ -196,7 +196,7 @@ size_t simt_smem_bytes(int BQ, int dim, int stage_rows, int n_stages_ring) {
 template <int BQ, int P>
 static cudaError_t launch_t(const SimtScanParams& p, int grid, size_t smem, cudaStream_t st) {
   auto kern = k_scan_simt<BQ, P>;
-  cudaError_t e = set_smem_attrs_once((const void*)kern, 232448);
+  cudaError_t e = set_smem_attrs_once((const void*)kern, kSimtMaxSmem);
   if (e != cudaSuccess) return e;
   kern<<<grid, kThreads, smem, st>>>(p);
   return cudaGetLastError();

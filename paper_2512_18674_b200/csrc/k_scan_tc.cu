@@ -559,6 +559,7 @@ remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int 
     t->why = "cuTensorMapEncodeTiled unavailable";
     return REMOE_OK;
   }
+  t->kn = TcKnobs::from_env();
   const cuuint64_t gdim[2] = {(cuuint64_t)dim, (cuuint64_t)n_rows};
   const cuuint64_t gstride[1] = {(cuuint64_t)row_stride * 2};
   const cuuint32_t box[2] = {(cuuint32_t)kBlockK, (cuuint32_t)kTileN};
@@ -566,7 +567,7 @@ remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int 
   CUresult r = ((EncodeTiledFn)fn)(reinterpret_cast<CUtensorMap*>(t->tmap_x), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                                    const_cast<uint16_t*>(x), gdim, gstride, box, estr,
                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                   tmap_promotion(),
+                                   t->kn.promotion(),
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) { t->why = "cuTensorMapEncodeTiled failed"; return REMOE_OK; }
   const int64_t n_tiles = (n_rows + kTileN - 1) / kTileN;
@@ -576,7 +577,12 @@ remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int 
   return REMOE_OK;
 }
 
-void tc_plan_destroy(TcPlan* t) { t->ok = false; }
+void tc_plan_destroy(TcPlan* t) {
+  t->ok = false;
+  if (t->stats_buf) cudaFree(t->stats_buf);
+  if (t->trace_buf) cudaFree(t->trace_buf);
+  t->stats_buf = t->trace_buf = nullptr;
+}
 
 template <int M, int P, int KR = 0>
 static cudaError_t launch_tc_t(const TcPlan* t, const TcArgs& a, dim3 grid, cudaStream_t st) {
@@ -591,9 +597,9 @@ static cudaError_t launch_tc_t(const TcPlan* t, const TcArgs& a, dim3 grid, cuda
     TcArgs& aa = const_cast<TcArgs&>(a);
     while (aa.cluster > 1 && ((grid.y % aa.cluster) != 0 ||
                               (int)(grid.x * grid.y / aa.cluster) >
-                                  max_active_clusters((const void*)kern, dim3(kThreads), smem, aa.cluster)))
+                                  max_active_clusters_cached((const void*)kern, dim3(kThreads), smem, aa.cluster)))
       aa.cluster >>= 1;
-    if (getenv("REMOE_VERBOSE"))
+    if (t->kn.verbose)
       fprintf(stderr, "[remoe] tc scan grid (%u,%u) cluster %d (max active clusters of 8/4/2: %d/%d/%d)\n",
               grid.x, grid.y, aa.cluster, max_active_clusters((const void*)kern, dim3(kThreads), smem, 8),
               max_active_clusters((const void*)kern, dim3(kThreads), smem, 4),
@@ -638,10 +644,11 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
   const int buf_bytes = k <= 32 ? 0 : kTcEpilogueThreads * 32 * topk_P(k) * 8;
   // a single slab stores only the 8-row atoms its queries need (more stages for small B)
   const int n_slabs_all = (bc + M - 1) / M;
-  const int SR = (n_slabs_all == 1 && !getenv("REMOE_TC_FULL_SLAB")) ? ((bc + 7) / 8) * 8 : M;
-  const bool smem_bufs = k > 32 && tc_stages(M, t->dim, buf_bytes, SR) >= 4 && !getenv("REMOE_TC_GLOBAL_BUFS");
+  const TcKnobs& kn = t->kn;
+  const int SR = (n_slabs_all == 1 && !kn.full_slab) ? ((bc + 7) / 8) * 8 : M;
+  const bool smem_bufs = k > 32 && tc_stages(M, t->dim, buf_bytes, SR) >= 4 && !kn.global_bufs;
   int nst = tc_stages(M, t->dim, smem_bufs ? buf_bytes : 0, SR);
-  if (const char* e = getenv("REMOE_TC_STAGES")) { const int v = atoi(e); if (v >= 2 && v < nst) nst = v; }
+  if (kn.stages >= 2 && kn.stages < nst) nst = kn.stages;
   // register top-k merges its two parity states in-CTA when the stage ring can hold them
   const int KR = k <= 1 ? 1 : k <= 2 ? 2 : k <= 4 ? 4 : k <= 8 ? 8 : k <= 16 ? 16 : 32;
   const bool in_cta = k <= 32 && (size_t)nst * kStageBytes >= (size_t)kTcEpilogueThreads * KR * 8;
@@ -672,24 +679,22 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
     a.out = lists + (size_t)s0 * ctas_per_slab * lists_per_cta * k;
     a.merge_in_cta = in_cta ? 1 : 0;
     a.smem_bufs = smem_bufs ? 1 : 0;
-    a.cluster = getenv("REMOE_NO_MULTICAST") ? 1 : 8;  // reduced to what fits in launch_tc_t
-    a.epi_sleep = getenv("REMOE_EPI_SLEEP") ? atoi(getenv("REMOE_EPI_SLEEP")) : 0;
+    a.cluster = kn.no_multicast ? 1 : 8;  // reduced to what fits in launch_tc_t
+    a.epi_sleep = kn.epi_sleep;
     a.xt = t->xt;
-    a.kb_order = kb_order_env();
+    a.kb_order = kn.kb_order;
     a.slab_rows = SR;
-    a.dbg = getenv("REMOE_TC_DBG") ? atoi(getenv("REMOE_TC_DBG")) : 0;
-    static unsigned long long* stats = nullptr;
-    if (getenv("REMOE_TC_STATS")) {
-      if (!stats) { cudaMalloc(&stats, 3 * 8); }
-      cudaMemsetAsync(stats, 0, 3 * 8, st);
-      a.stats = stats;
+    a.dbg = kn.dbg;
+    if (kn.stats) {  // debug counters (this plan's buffer)
+      if (!t->stats_buf && cudaMalloc(&t->stats_buf, 3 * 8) != cudaSuccess) return REMOE_ERR_OOM;
+      cudaMemsetAsync(t->stats_buf, 0, 3 * 8, st);
+      a.stats = t->stats_buf;
     }
-    static unsigned long long* trace = nullptr;
     const int n_cta = ctas_per_slab * ns;
-    if (getenv("REMOE_TC_TRACE")) {  // debug: per-CTA globaltimer stamps of the launch phases
-      if (!trace) cudaMalloc(&trace, (size_t)148 * 64 * 16 * 8);
-      cudaMemsetAsync(trace, 0, (size_t)n_cta * 16 * 8, st);
-      a.trace = trace;
+    if (kn.trace) {  // debug: per-CTA globaltimer stamps of the launch phases (this plan's buffer)
+      if (!t->trace_buf && cudaMalloc(&t->trace_buf, (size_t)t->grid * 16 * 8) != cudaSuccess) return REMOE_ERR_OOM;
+      cudaMemsetAsync(t->trace_buf, 0, (size_t)n_cta * 16 * 8, st);
+      a.trace = t->trace_buf;
     }
     const dim3 g((unsigned)ctas_per_slab, (unsigned)ns);
     cudaError_t e = (M == 128) ? launch_tc_m<128>(t, a, g, st) : launch_tc_m<64>(t, a, g, st);

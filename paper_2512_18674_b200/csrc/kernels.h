@@ -26,6 +26,7 @@ struct SimtScanParams {
   uint64_t* out;          // [nq][grid][k]
 };
 size_t simt_smem_bytes(int BQ, int dim, int stage_rows, int n_stages_ring);
+constexpr int kSimtMaxSmem = 232448;  // opt-in dynamic shared memory per CTA (227 KB)
 cudaError_t launch_scan_simt(const SimtScanParams& p, int BQ, int grid, cudaStream_t st);
 
 // S2+S3, tensor-core (tcgen05) variant; see k_scan_tc.cu.
@@ -35,12 +36,15 @@ cudaError_t launch_scan_simt(const SimtScanParams& p, int BQ, int grid, cudaStre
 cudaError_t launch_norms(const uint16_t* x, int64_t n, int dim, float* out, cudaStream_t st,
                          unsigned long long* zero_u64 = nullptr, int64_t zero_stride = 0);
 
-// S6 + S7 arguments.  mode 0: rows come from the local table act[(gid - offset) * LE];
-// mode 1: rows come from rows[(b * k + r) * LE] (multi-GPU gathered winners).
+// S6 + S7 arguments.  mode 0: every winner's row comes from the local table
+// act[(gid - offset) * LE] (one GPU: this rank holds every row).  mode 2 (multi-GPU
+// partial prediction): only the winners this rank owns (offset <= gid < offset + n_local)
+// contribute, in r-ascending order; the others are skipped, so pred receives this rank's
+// partial P_g = sum over owned r of w_r S~_{id_r} (SURVEY §8(e) exchange 2).
 struct FinalizeArgs {
   const float* act;
   int64_t offset;
-  const float* rows;
+  int64_t n_local;
   int mode;
   int64_t LE;
   float T;
@@ -60,14 +64,12 @@ cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride
                          const unsigned long long* lower = nullptr, const FinalizeArgs* fin = nullptr,
                          int list_len = -1);
 
-// S6 + S7 as a separate kernel (multi-GPU path, after the row exchange).
-cudaError_t launch_finalize(const uint64_t* top, int B, int k, const float* act, int64_t offset,
-                            const float* rows, int mode, int64_t LE, float temperature,
-                            int64_t* ids, float* scores, float* pred, cudaStream_t st);
+// S6 + S7 as a separate kernel (tree search path with world == 1).
+cudaError_t launch_finalize(const uint64_t* top, int B, int k, const FinalizeArgs& f, cudaStream_t st);
 
-// Multi-GPU S7 helper: rows[b][r] = act[gid - offset] if this rank owns gid, else 0.
-cudaError_t launch_gather_rows(const uint64_t* top, int B, int k, const float* act, int64_t offset,
-                               int64_t n_local, int64_t LE, float* rows, cudaStream_t st);
+// Multi-GPU S7 combine: out[i] = sum_{g = 0..G-1} parts[g * part_stride + i] for i < n, g
+// ascending (a fixed order: every rank and every batch position gets the same bits).
+cudaError_t launch_psum(const float* parts, int G, int64_t part_stride, int64_t n, float* out, cudaStream_t st);
 
 // S8: cold mask of the n_cold smallest entries per (query, layer).
 cudaError_t launch_plan(const float* pred, int B, int L, int E, int n_cold, uint8_t* mask,

@@ -1,19 +1,25 @@
 // runtime.cu -- the C ABI (include/remoe.h): handle, validation, workspaces,
-// kernel selection, the per-query launch sequence and the NCCL exchange.
+// kernel selection, the per-query launch sequence and the multi-rank exchange.
 //
-// Query sequence per chunk of <= max_batch queries (SURVEY §3c):
-//   k_norms(Q)                                   S1
-//   k_scan_{simt|tc}                             S2+S3  (per-CTA top-k lists)
-//   k_merge(n_cta lists -> local top-k)          S4
-//   [world > 1] ncclAllGather(local keys) + k_merge(G lists -> global top-k)   S5
-//   [pred]  world == 1: k_finalize(mode 0, rows read from the local table)    S6+S7
-//           world >  1: k_gather_rows (owned winners, zeros elsewhere)
-//                       + ncclAllReduce(sum): exactly one non-zero term per
-//                         element, so the sum is exact and order-free
-//                       + k_finalize(mode 1)  -> bit-identical to world == 1
+// Query sequence per chunk of <= max_batch queries (SURVEY §3c, §8(a)):
+//   k_norms(Q)                                     S1
+//   k_scan_{simt|tc|pair}                          S2+S3  (per-CTA top-k lists)
+//   k_merge(n_cta lists -> local top-k)            S4     (world == 1: + S6+S7 fused)
+//   world > 1:
+//     exchange 1: all-gather of the local top-k keys [G][B][k]
+//     k_merge(G lists -> global top-k) + fused S6 + partial S7: every rank writes the
+//       same ids/scores and P_g = sum over the winners it OWNS (r ascending)       S5-S7
+//     exchange 2: all-gather of the partials [G][B][L*E] (small) or, above
+//       xchg_ag_max bytes, an all-to-all by query slice + broadcast of the slices
+//     k_psum: P = P_0 + P_1 + ... + P_{G-1} in rank order (identical bits on every rank
+//       and at every batch position; ncclAllReduce's ring order would not give that)
+// The exchanges run over NCCL between processes, or -- for a loopback group (test
+// harness: G handles of one process on one device) -- as device copies; both drive
+// the same stage functions below.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -78,7 +84,31 @@ struct DeviceGuard {
   }
 };
 
+// NVTX range for profiler timelines (header-only nvtx3; a no-op without a tool attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
+// Balanced contiguous slice g of n items over G owners: [lo, lo + cnt).
+inline void slice_of(int n, int G, int g, int* lo, int* cnt) {
+  const int a = (int)((int64_t)n * g / G), b = (int)((int64_t)n * (g + 1) / G);
+  *lo = a;
+  *cnt = b - a;
+}
+
+constexpr int kGraphCache = 8;  // cached device-query graphs per handle (distinct buffer sets)
+
 }  // namespace
+
+struct remoe_sps;
+
+// A loopback group: `world` handles built in one process on one device that act as the
+// ranks of one sharded store; their exchanges are device copies (remoe_sps_query_group).
+struct remoe_group {
+  int world = 0;
+  std::vector<remoe_sps*> members;  // by rank; nullptr until that rank is built
+};
 
 struct remoe_sps {
   remoe_sps_config_t cfg{};
@@ -88,6 +118,7 @@ struct remoe_sps {
   int grid_simt = 0;
   int grid_tc = 0;
   int stage_rows = 0;
+  remoe_group* group = nullptr;  // loopback group membership (world > 1 without NCCL)
   // store
   uint16_t* x = nullptr;
   uint16_t* xt = nullptr;  // tiled copy for the tensor-core scan (or nullptr)
@@ -99,9 +130,12 @@ struct remoe_sps {
   uint64_t* cand_buf = nullptr;
   uint64_t* lists = nullptr;
   uint64_t* local_top = nullptr;
-  uint64_t* gathered = nullptr;
+  uint64_t* gathered = nullptr;    // [world][max_batch][max_k] (world > 1)
   uint64_t* global_top = nullptr;
-  float* rows = nullptr;
+  float* part = nullptr;           // [max_batch][LE] this rank's partial prediction (world > 1)
+  float* part_all = nullptr;       // gathered partials / all-to-all receive buffer (world > 1)
+  size_t part_all_floats = 0;
+  size_t xchg_ag_max = 32u << 20;  // exchange 2 by all-gather while world*B*LE*4 <= this
   // host-path staging
   uint16_t* hq = nullptr;
   int64_t* hids = nullptr;
@@ -133,6 +167,7 @@ struct remoe_sps {
   int force_kernel = 0;
   int last_kernel = 0;
   int pair_min_b = remoe::kPairMinB;  // auto: batches >= this use the CTA-pair scan
+  bool use_graphs = true;             // REMOE_NO_GRAPH=1 at build turns the query graphs off
   int last_launches = 0;
   size_t device_bytes = 0;
   std::vector<void*> allocs;
@@ -153,10 +188,33 @@ struct remoe_sps {
       h2d = d2h_ids = d2h_sc = d2h_pred = nullptr; launches = 0;
     }
   } hg;
-  // the graph is captured and replayed on a library stream (the caller's may be the legacy
-  // default stream, which cannot be captured), ordered after the caller's stream by an event
+  // CUDA graphs of the device-buffer query (remoe_sps_query, world == 1, one chunk): one
+  // per (buffers, B, k) with LRU replacement.  The caller's buffers are baked into the
+  // kernel nodes, so a graph is reused only for the same pointers.
+  struct DevGraph {
+    const void* q = nullptr;
+    const void* ids = nullptr;
+    const void* scores = nullptr;
+    const void* pred = nullptr;
+    int B = -1, k = -1, kernel = -1;
+    cudaGraphExec_t exec = nullptr;
+    int launches = 0;
+    uint64_t used = 0;
+    void reset() {
+      if (exec) cudaGraphExecDestroy(exec);
+      exec = nullptr; q = ids = scores = pred = nullptr; B = k = kernel = -1; launches = 0; used = 0;
+    }
+  } dg[kGraphCache];
+  uint64_t dg_clock = 0;
+  void reset_graphs() {
+    hg.reset();
+    for (auto& g : dg) g.reset();
+  }
+  // the graphs are captured and replayed on a library stream (the caller's may be the legacy
+  // default stream, which cannot be captured), ordered after / before the caller's stream
+  // by events
   cudaStream_t gst = nullptr;
-  cudaEvent_t gev = nullptr;
+  cudaEvent_t gev = nullptr, gev_done = nullptr;
   // live scan timing (remoe_sps_profile)
   bool prof = false;
   std::vector<cudaEvent_t> prof_ev;  // pairs (start, end)
@@ -201,8 +259,9 @@ struct remoe_sps {
     return REMOE_OK;
   }
   void release() {
-    hg.reset();
+    reset_graphs();
     if (gev) { cudaEventDestroy(gev); gev = nullptr; }
+    if (gev_done) { cudaEventDestroy(gev_done); gev_done = nullptr; }
     if (gst) { cudaStreamDestroy(gst); gst = nullptr; }
     for (void* p : allocs) cudaFree(p);
     allocs.clear();
@@ -213,6 +272,11 @@ struct remoe_sps {
     n_seeds = 0;
     if (has_tree) { remoe::tree_free(&tree); has_tree = false; }
     if (comm) { ncclCommDestroy(comm); comm = nullptr; }
+    if (group) {
+      if (cfg.rank >= 0 && cfg.rank < (int)group->members.size() && group->members[cfg.rank] == this)
+        group->members[cfg.rank] = nullptr;
+      group = nullptr;
+    }
   }
 };
 
@@ -253,8 +317,58 @@ remoe_status_t remoe_nccl_unique_id(uint8_t out[128]) {
   return REMOE_OK;
 }
 
-static remoe_status_t check_config(const remoe_sps_config_t* c) {
+remoe_status_t remoe_loopback_group_create(int32_t world, remoe_group_t* out) {
+  if (!out) return fail(REMOE_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (world < 1 || world > 1024) return fail(REMOE_ERR_INVALID_ARG, "need 1 <= world <= 1024");
+  remoe_group* g = new (std::nothrow) remoe_group();
+  if (!g) return fail(REMOE_ERR_OOM, "host allocation failed");
+  g->world = world;
+  g->members.assign(world, nullptr);
+  *out = g;
+  return REMOE_OK;
+}
+
+remoe_status_t remoe_loopback_group_destroy(remoe_group_t g) {
+  if (!g) return REMOE_OK;
+  for (remoe_sps* m : g->members)
+    if (m) return fail(REMOE_ERR_STATE, "destroy the group's handles first");
+  delete g;
+  return REMOE_OK;
+}
+
+// Checks that cannot wait for the multi-rank agreement (a rank failing them cannot even
+// join the group).  Everything else is checked by check_local after the NCCL
+// communicator exists, so that every rank fails together (remoe_sps_build's agreement).
+static remoe_status_t check_join(const remoe_sps_config_t* c) {
   if (!c) return fail(REMOE_ERR_INVALID_ARG, "cfg is NULL");
+  if (c->world < 1 || c->rank < 0 || c->rank >= c->world)
+    return fail(REMOE_ERR_INVALID_ARG, "need 0 <= rank < world");
+  const bool lb = c->loopback_group != nullptr;
+  if (c->world == 1 && (c->nccl_unique_id != nullptr || lb))
+    return fail(REMOE_ERR_INVALID_ARG, "world == 1 takes neither an NCCL id nor a loopback group");
+  if (c->world > 1 && ((c->nccl_unique_id != nullptr) == lb))
+    return fail(REMOE_ERR_INVALID_ARG, "world > 1 needs exactly one of nccl_unique_id / loopback_group");
+  if (lb) {
+    const remoe_group* g = static_cast<const remoe_group*>(c->loopback_group);
+    if (g->world != c->world) return fail(REMOE_ERR_INVALID_ARG, "loopback group world %d != cfg world %d",
+                                          g->world, c->world);
+    if (g->members[c->rank] != nullptr) return fail(REMOE_ERR_STATE, "rank %d of the loopback group is taken", c->rank);
+  }
+  return REMOE_OK;
+}
+
+static remoe_status_t check_device(const remoe_sps_config_t* c) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(REMOE_ERR_CUDA, "no CUDA device visible");
+  }
+  if (c->device < 0 || c->device >= ndev) return fail(REMOE_ERR_INVALID_ARG, "device out of range");
+  return REMOE_OK;
+}
+
+static remoe_status_t check_local(const remoe_sps_config_t* c, const void* emb, const void* act) {
   if (c->n_local < 1) return fail(REMOE_ERR_INVALID_ARG, "n_local must be >= 1");
   if (c->global_offset < 0) return fail(REMOE_ERR_INVALID_ARG, "global_offset must be >= 0");
   if (c->global_offset + c->n_local > 0xFFFFFFFELL)
@@ -269,47 +383,15 @@ static remoe_status_t check_config(const remoe_sps_config_t* c) {
   if (c->max_batch < 1) return fail(REMOE_ERR_INVALID_ARG, "max_batch must be >= 1");
   if (c->max_k < 1) return fail(REMOE_ERR_INVALID_ARG, "max_k must be >= 1");
   if (c->max_k > 256) return fail(REMOE_ERR_UNSUPPORTED, "max_k > 256");
-  if (c->world < 1 || c->rank < 0 || c->rank >= c->world)
-    return fail(REMOE_ERR_INVALID_ARG, "need 0 <= rank < world");
-  if ((c->world == 1) != (c->nccl_unique_id == nullptr))
-    return fail(REMOE_ERR_INVALID_ARG, "nccl_unique_id must be NULL iff world == 1");
+  if (!emb || !act) return fail(REMOE_ERR_INVALID_ARG, "emb/act is NULL");
   return REMOE_OK;
 }
 
-static remoe_status_t build_impl(remoe_sps* h, const uint16_t* emb, const float* act) {
+// Everything of the build that is local to this rank: the store, its norms and validation,
+// the tensor-core plans and the workspaces.
+static remoe_status_t build_local(remoe_sps* h, const uint16_t* emb, const float* act, cudaStream_t st) {
   const remoe_sps_config_t& c = h->cfg;
-  CUDA_TRY(cudaSetDevice(c.device));
-  CUDA_TRY(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, c.device));
-  h->LE = (int64_t)c.n_layers * c.n_experts;
-  cudaStream_t st = nullptr;
-  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamDestroy(s); } } sg{st};
-
-  // ---- bootstrap + shard tiling check
-  if (c.world > 1) {
-    ncclUniqueId id;
-    std::memcpy(&id, c.nccl_unique_id, sizeof id);
-    NCCL_TRY(ncclCommInitRank(&h->comm, c.world, id, c.rank));
-    int64_t* d = nullptr;
-    ST_TRY(h->alloc((void**)&d, sizeof(int64_t) * 2 * (c.world + 1)));
-    int64_t mine[2] = {c.global_offset, c.n_local};
-    CUDA_TRY(cudaMemcpyAsync(d, mine, sizeof mine, cudaMemcpyHostToDevice, st));
-    NCCL_TRY(ncclAllGather(d, d + 2, 2, ncclInt64, h->comm, st));
-    std::vector<int64_t> all(2 * c.world);
-    CUDA_TRY(cudaMemcpyAsync(all.data(), d + 2, sizeof(int64_t) * 2 * c.world, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    int64_t expect = 0;
-    for (int g = 0; g < c.world; ++g) {
-      if (all[2 * g] != expect)
-        return fail(REMOE_ERR_INVALID_ARG, "shards do not tile [0, N): rank %d offset %lld, expected %lld",
-                    g, (long long)all[2 * g], (long long)expect);
-      expect += all[2 * g + 1];
-    }
-    h->n_total = expect;
-  } else {
-    h->n_total = c.n_local;
-  }
-
+  ST_TRY(check_local(&c, emb, act));
   // ---- store
   const size_t xbytes = (size_t)c.n_local * c.dim * 2;
   const size_t abytes = (size_t)c.n_local * h->LE * 4;
@@ -379,13 +461,23 @@ static remoe_status_t build_impl(remoe_sps* h, const uint16_t* emb, const float*
   if (const char* e = getenv("REMOE_SEED_MIN_B")) h->seed_min_b = atoi(e);
   if (const char* e = getenv("REMOE_SEED_KS")) h->seed_ks = std::max(0, std::min(32, atoi(e)));
   if (const char* e = getenv("REMOE_PAIR_MIN_B")) h->pair_min_b = atoi(e);
+  if (const char* e = getenv("REMOE_NO_GRAPH")) h->use_graphs = atoi(e) == 0;
+  if (const char* e = getenv("REMOE_XCHG_AG_MAX")) h->xchg_ag_max = (size_t)std::max(0LL, atoll(e));
   ST_TRY(h->alloc((void**)&h->cand_buf, cand_lanes * capmax * 8));
   ST_TRY(h->alloc((void**)&h->lists, (size_t)mb * lists_max * c.max_k * 8));
   ST_TRY(h->alloc((void**)&h->local_top, (size_t)mb * c.max_k * 8));
   ST_TRY(h->alloc((void**)&h->global_top, (size_t)mb * c.max_k * 8));
   if (c.world > 1) {
-    ST_TRY(h->alloc((void**)&h->gathered, (size_t)c.world * mb * c.max_k * 8));
-    ST_TRY(h->alloc((void**)&h->rows, (size_t)mb * c.max_k * h->LE * 4));
+    // exchange workspaces: keys [G][mb][max_k]; this rank's partial P
+    // [mb][LE]; the gathered partials [G][mb][LE] when they fit xchg_ag_max, and always
+    // the all-to-all receive slices [G][ceil(mb / G)][LE]
+    const size_t G = (size_t)c.world, LE = (size_t)h->LE;
+    ST_TRY(h->alloc((void**)&h->gathered, G * mb * c.max_k * 8));
+    ST_TRY(h->alloc((void**)&h->part, (size_t)mb * LE * 4));
+    const size_t a2a = G * ((mb + G - 1) / G) * LE;
+    const size_t ag = std::min(G * mb * LE, h->xchg_ag_max / 4);
+    h->part_all_floats = std::max(a2a, ag);
+    ST_TRY(h->alloc((void**)&h->part_all, h->part_all_floats * 4));
   }
   ST_TRY(h->alloc((void**)&h->hq, (size_t)mb * c.dim * 2));
   ST_TRY(h->alloc((void**)&h->hids, (size_t)mb * c.max_k * 8));
@@ -401,16 +493,83 @@ static remoe_status_t build_impl(remoe_sps* h, const uint16_t* emb, const float*
   return REMOE_OK;
 }
 
+// NCCL ranks agree on the build: every rank contributes (offset, n_local, status); if any
+// rank failed, every rank fails (none is left waiting in a later collective), otherwise
+// the shards must tile [0, N) in rank order.
+static remoe_status_t agree_build(remoe_sps* h, remoe_status_t local, cudaStream_t st) {
+  const remoe_sps_config_t& c = h->cfg;
+  const std::string local_err = g_err;
+  int64_t* d = nullptr;
+  const size_t bytes = sizeof(int64_t) * 3 * (c.world + 1);
+  if (cudaMalloc(&d, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(REMOE_ERR_OOM, "agreement buffer");  // cannot take part: peers will see NCCL errors
+  }
+  int64_t mine[3] = {c.global_offset, c.n_local, (int64_t)local};
+  std::vector<int64_t> all(3 * c.world);
+  cudaError_t ce = cudaMemcpyAsync(d, mine, sizeof mine, cudaMemcpyHostToDevice, st);
+  ncclResult_t nr = ce == cudaSuccess ? ncclAllGather(d, d + 3, 3, ncclInt64, h->comm, st) : ncclSuccess;
+  if (ce == cudaSuccess && nr == ncclSuccess)
+    ce = cudaMemcpyAsync(all.data(), d + 3, sizeof(int64_t) * 3 * c.world, cudaMemcpyDeviceToHost, st);
+  if (ce == cudaSuccess && nr == ncclSuccess) ce = cudaStreamSynchronize(st);
+  cudaFree(d);
+  if (local != REMOE_OK) {
+    g_err = local_err;
+    return local;
+  }
+  if (nr != ncclSuccess) return fail(REMOE_ERR_NCCL, "build agreement: %s", ncclGetErrorString(nr));
+  if (ce != cudaSuccess) return fail(REMOE_ERR_CUDA, "build agreement: %s", cudaGetErrorString(ce));
+  for (int g = 0; g < c.world; ++g)
+    if (all[3 * g + 2] != REMOE_OK)
+      return fail((remoe_status_t)all[3 * g + 2], "rank %d failed its build (%s); every rank fails", g,
+                  remoe_status_string((remoe_status_t)all[3 * g + 2]));
+  int64_t expect = 0;
+  for (int g = 0; g < c.world; ++g) {
+    if (all[3 * g] != expect)
+      return fail(REMOE_ERR_INVALID_ARG, "shards do not tile [0, N): rank %d offset %lld, expected %lld",
+                  g, (long long)all[3 * g], (long long)expect);
+    expect += all[3 * g + 1];
+  }
+  h->n_total = expect;
+  return REMOE_OK;
+}
+
+static remoe_status_t build_impl(remoe_sps* h, const uint16_t* emb, const float* act) {
+  const remoe_sps_config_t& c = h->cfg;
+  CUDA_TRY(cudaSetDevice(c.device));
+  CUDA_TRY(cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, c.device));
+  h->LE = (int64_t)c.n_layers * c.n_experts;
+  cudaStream_t st = nullptr;
+  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard { cudaStream_t s; ~StreamGuard() { cudaStreamDestroy(s); } } sg{st};
+  if (c.world > 1 && c.loopback_group == nullptr) {
+    // the communicator first: a rank whose local build fails below still takes part in
+    // the agreement, so no peer is left blocked in a collective
+    ncclUniqueId id;
+    std::memcpy(&id, c.nccl_unique_id, sizeof id);
+    NCCL_TRY(ncclCommInitRank(&h->comm, c.world, id, c.rank));
+    return agree_build(h, build_local(h, emb, act, st), st);
+  }
+  ST_TRY(build_local(h, emb, act, st));
+  if (c.loopback_group) {
+    h->group = static_cast<remoe_group*>(const_cast<void*>(c.loopback_group));
+    h->group->members[c.rank] = h;
+    h->n_total = 0;  // known once every member is built (checked by remoe_sps_query_group)
+  } else {
+    h->n_total = c.n_local;
+  }
+  return REMOE_OK;
+}
+
 remoe_status_t remoe_sps_build(const remoe_sps_config_t* cfg, const uint16_t* emb_bf16,
                                const float* act, remoe_sps_t* out) {
   if (!out) return fail(REMOE_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
-  ST_TRY(check_config(cfg));
-  if (!emb_bf16 || !act) return fail(REMOE_ERR_INVALID_ARG, "emb/act is NULL");
-  int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
-    return fail(REMOE_ERR_CUDA, "no CUDA device visible");
-  if (cfg->device < 0 || cfg->device >= ndev) return fail(REMOE_ERR_INVALID_ARG, "device out of range");
+  ST_TRY(check_join(cfg));
+  // single-process builds check everything up front, before any CUDA call; NCCL ranks
+  // check the rest after the communicator exists (build_impl's agreement)
+  if (cfg->world == 1 || cfg->loopback_group) ST_TRY(check_local(cfg, emb_bf16, act));
+  ST_TRY(check_device(cfg));
   remoe_sps* h = new (std::nothrow) remoe_sps();
   if (!h) return fail(REMOE_ERR_OOM, "host allocation failed");
   h->cfg = *cfg;
@@ -426,42 +585,15 @@ remoe_status_t remoe_sps_build(const remoe_sps_config_t* cfg, const uint16_t* em
   return s;
 }
 
-// S5..S7 from h->local_top (one sorted key list of length k per query).  world == 1:
-// S6+S7 directly; world > 1: all-gather + merge, then the owned-winner row exchange.
-static remoe_status_t post_local_top(remoe_sps* h, int bc, int k, int64_t* ids, float* scores, float* pred,
-                                     cudaStream_t st, int* launches) {
-  const remoe_sps_config_t& c = h->cfg;
-  const remoe::FinalizeArgs fin_local{h->act, c.global_offset, nullptr, 0, h->LE, c.temperature,
-                                      ids, scores, pred};
-  if (c.world == 1) {
-    CUDA_TRY(remoe::launch_finalize(h->local_top, bc, k, h->act, c.global_offset, nullptr, 0, h->LE,
-                                    c.temperature, ids, scores, pred, st));
-    ++*launches;
-    return REMOE_OK;
-  }
-  // ---- S5: every rank gathers all ranks' local top-k keys and runs the same merge
-  NCCL_TRY(ncclAllGather(h->local_top, h->gathered, (size_t)bc * k, ncclUint64, h->comm, st));
-  if (!pred) {
-    CUDA_TRY(remoe::launch_merge(h->gathered, bc, c.world, k, (int64_t)bc * k, k, h->global_top, st, nullptr,
-                                 nullptr, &fin_local));
-    ++*launches;
-    return REMOE_OK;
-  }
-  CUDA_TRY(remoe::launch_merge(h->gathered, bc, c.world, k, (int64_t)bc * k, k, h->global_top, st));
-  // ---- S6 + S7: owners contribute their winner rows (zeros elsewhere); one exact
-  // all-reduce gives every rank every winner row, then the same r-ascending sum
-  CUDA_TRY(remoe::launch_gather_rows(h->global_top, bc, k, h->act, c.global_offset, c.n_local, h->LE,
-                                     h->rows, st));
-  NCCL_TRY(ncclAllReduce(h->rows, h->rows, (size_t)bc * k * h->LE, ncclFloat, ncclSum, h->comm, st));
-  CUDA_TRY(remoe::launch_finalize(h->global_top, bc, k, h->act, c.global_offset, h->rows, 1, h->LE,
-                                  c.temperature, ids, scores, pred, st));
-  *launches += 3;
-  return REMOE_OK;
-}
+}  // extern "C"
 
+// ------------------------------------------------------------------ query stages
 
-static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k, int64_t* ids,
-                                  float* scores, float* pred, cudaStream_t st, int* launches) {
+// S1-S4 on this rank's shard: query norms, [threshold seeding], the scan, and the merge of
+// the per-CTA lists.  With `fin` (world == 1) the merge CTA goes on to S5-S7 itself (ids,
+// scores, prediction); otherwise the local top-k keys land in h->local_top.
+static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k, const remoe::FinalizeArgs* fin,
+                                 cudaStream_t st, int* launches) {
   const remoe_sps_config_t& c = h->cfg;
   CUDA_TRY(remoe::launch_norms(q, bc, c.dim, h->qnorm, st, h->gthr, c.max_batch));
   ++*launches;
@@ -478,9 +610,14 @@ static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k
   CUDA_TRY(h->prof_mark(st, true));
   if (which == 1) {
     grid = h->grid_simt;
-    const int BQ = bc >= 8 ? 8 : bc >= 4 ? 4 : bc >= 2 ? 2 : 1;
-    const int NST = std::max(2, std::min(6, (int)((210 * 1024 - (size_t)BQ * c.dim * 4) /
-                                                   ((size_t)h->stage_rows * c.dim * 2))));
+    int BQ = bc >= 8 ? 8 : bc >= 4 ? 4 : bc >= 2 ? 2 : 1;
+    // the query slab (BQ x D fp32) and >= 2 stages must fit the opt-in shared memory
+    while (BQ > 1 && remoe::simt_smem_bytes(BQ, c.dim, h->stage_rows, 2) > (size_t)remoe::kSimtMaxSmem) BQ >>= 1;
+    if (remoe::simt_smem_bytes(BQ, c.dim, h->stage_rows, 2) > (size_t)remoe::kSimtMaxSmem)
+      return fail(REMOE_ERR_UNSUPPORTED, "streaming scan: D = %d does not fit shared memory", c.dim);
+    int NST = std::max(2, std::min(6, (int)((210 * 1024 - std::min<size_t>(210 * 1024, (size_t)BQ * c.dim * 4)) /
+                                            ((size_t)h->stage_rows * c.dim * 2))));
+    while (NST > 2 && remoe::simt_smem_bytes(BQ, c.dim, h->stage_rows, NST) > (size_t)remoe::kSimtMaxSmem) --NST;
     for (int s0 = 0; s0 < bc; s0 += BQ) {
       remoe::SimtScanParams p{};
       p.x = h->x; p.xnorm = h->xnorm; p.n_rows = c.n_local; p.gid_offset = c.global_offset;
@@ -547,21 +684,167 @@ static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k
   // ---- S4 (+ S5..S7 fused when world == 1).  gthr[b] holds a lower bound of the
   // final k-th best key (every published value is some state's own k-th best or a
   // seeded strict bound), so the merge drops every key below it.
-  const remoe::FinalizeArgs fin_local{h->act, c.global_offset, nullptr, 0, h->LE, c.temperature,
-                                      ids, scores, pred};
-  if (c.world == 1) {
-    CUDA_TRY(remoe::launch_merge(h->lists, bc, grid, (int64_t)grid * k, k, k, h->local_top, st, nullptr,
-                                 h->gthr, &fin_local));
-    ++*launches;
+  CUDA_TRY(remoe::launch_merge(h->lists, bc, grid, (int64_t)grid * k, k, k, h->local_top, st, nullptr,
+                               h->gthr, fin));
+  ++*launches;
+  return REMOE_OK;
+}
+
+// S5 + S6 + partial S7 (world > 1): merge the G gathered key lists into the global top-k
+// (every rank runs the same merge on the same keys, so every rank writes the same ids and
+// scores), softmax weights, and this rank's partial prediction from the winners it owns.
+static remoe_status_t stage_merge(remoe_sps* h, int bc, int k, int64_t* ids, float* scores, bool want_pred,
+                                  cudaStream_t st, int* launches) {
+  const remoe_sps_config_t& c = h->cfg;
+  const remoe::FinalizeArgs f{h->act, c.global_offset, c.n_local, 2, h->LE, c.temperature, ids, scores,
+                              want_pred ? h->part : nullptr};
+  CUDA_TRY(remoe::launch_merge(h->gathered, bc, c.world, k, (int64_t)bc * k, k, h->global_top, st, nullptr,
+                               nullptr, &f));
+  ++*launches;
+  return REMOE_OK;
+}
+
+// Exchange-2 layout: all-gather of whole partials while world * B * LE * 4 <= xchg_ag_max.
+static bool xchg_allgather(const remoe_sps* h, int bc) {
+  const size_t n = (size_t)h->cfg.world * bc * h->LE;
+  return n * 4 <= h->xchg_ag_max && n <= h->part_all_floats;
+}
+
+// S7 combine: pred = sum of the G partials in rank order.  All-gather layout: the whole
+// batch; all-to-all layout: this rank's query slice (broadcast afterwards).
+static remoe_status_t stage_combine(remoe_sps* h, int bc, float* pred, cudaStream_t st, int* launches) {
+  const int G = h->cfg.world;
+  const int64_t LE = h->LE;
+  if (xchg_allgather(h, bc)) {
+    CUDA_TRY(remoe::launch_psum(h->part_all, G, (int64_t)bc * LE, (int64_t)bc * LE, pred, st));
+  } else {
+    int lo, cnt;
+    slice_of(bc, G, h->cfg.rank, &lo, &cnt);
+    const int cap = (bc + G - 1) / G;
+    CUDA_TRY(remoe::launch_psum(h->part_all, G, (int64_t)cap * LE, (int64_t)cnt * LE, pred + (int64_t)lo * LE, st));
+  }
+  ++*launches;
+  return REMOE_OK;
+}
+
+enum class Xchg { Keys, PartsAllGather, PartsAllToAll, SlicesBroadcast };
+
+// One exchange step for the ranks in hs[0..nh): over NCCL (one handle of this process,
+// nh == 1) or, for a loopback group (all world handles, nh == world), as device copies
+// of exactly the bytes NCCL would move.
+static remoe_status_t exchange(remoe_sps* const* hs, int nh, Xchg x, int bc, int k, float* const* pred,
+                               cudaStream_t st) {
+  remoe_sps* h0 = hs[0];
+  const int G = h0->cfg.world;
+  const int64_t LE = h0->LE;
+  const int cap = (bc + G - 1) / G;
+  if (h0->comm) {
+    remoe_sps* h = h0;
+    switch (x) {
+      case Xchg::Keys:
+        NCCL_TRY(ncclAllGather(h->local_top, h->gathered, (size_t)bc * k, ncclUint64, h->comm, st));
+        break;
+      case Xchg::PartsAllGather:
+        NCCL_TRY(ncclAllGather(h->part, h->part_all, (size_t)bc * LE, ncclFloat, h->comm, st));
+        break;
+      case Xchg::PartsAllToAll: {
+        int lo_me, cnt_me;
+        slice_of(bc, G, h->cfg.rank, &lo_me, &cnt_me);
+        NCCL_TRY(ncclGroupStart());
+        for (int g = 0; g < G; ++g) {
+          int lo, cnt;
+          slice_of(bc, G, g, &lo, &cnt);
+          if (cnt > 0) NCCL_TRY(ncclSend(h->part + (size_t)lo * LE, (size_t)cnt * LE, ncclFloat, g, h->comm, st));
+          if (cnt_me > 0)
+            NCCL_TRY(ncclRecv(h->part_all + (size_t)g * cap * LE, (size_t)cnt_me * LE, ncclFloat, g, h->comm, st));
+        }
+        NCCL_TRY(ncclGroupEnd());
+        break;
+      }
+      case Xchg::SlicesBroadcast:
+        NCCL_TRY(ncclGroupStart());
+        for (int g = 0; g < G; ++g) {
+          int lo, cnt;
+          slice_of(bc, G, g, &lo, &cnt);
+          if (cnt > 0)
+            NCCL_TRY(ncclBroadcast(pred[0] + (size_t)lo * LE, pred[0] + (size_t)lo * LE, (size_t)cnt * LE, ncclFloat,
+                                   g, h->comm, st));
+        }
+        NCCL_TRY(ncclGroupEnd());
+        break;
+    }
     return REMOE_OK;
   }
-  CUDA_TRY(remoe::launch_merge(h->lists, bc, grid, (int64_t)grid * k, k, k, h->local_top, st, nullptr,
-                               h->gthr));
-  ++*launches;
-  return post_local_top(h, bc, k, ids, scores, pred, st, launches);
+  if (nh != G) return fail(REMOE_ERR_STATE, "loopback exchange needs all %d ranks", G);
+  const cudaMemcpyKind dd = cudaMemcpyDeviceToDevice;
+  for (int m = 0; m < G; ++m) {
+    remoe_sps* hm = hs[m];
+    for (int p = 0; p < G; ++p) {
+      const remoe_sps* hp = hs[p];
+      switch (x) {
+        case Xchg::Keys:
+          CUDA_TRY(cudaMemcpyAsync(hm->gathered + (size_t)p * bc * k, hp->local_top, (size_t)bc * k * 8, dd, st));
+          break;
+        case Xchg::PartsAllGather:
+          CUDA_TRY(cudaMemcpyAsync(hm->part_all + (size_t)p * bc * LE, hp->part, (size_t)bc * LE * 4, dd, st));
+          break;
+        case Xchg::PartsAllToAll: {
+          int lo, cnt;
+          slice_of(bc, G, m, &lo, &cnt);  // rank m receives its slice from every rank p
+          if (cnt > 0)
+            CUDA_TRY(cudaMemcpyAsync(hm->part_all + (size_t)p * cap * LE, hp->part + (size_t)lo * LE,
+                                     (size_t)cnt * LE * 4, dd, st));
+          break;
+        }
+        case Xchg::SlicesBroadcast: {
+          int lo, cnt;
+          slice_of(bc, G, p, &lo, &cnt);  // rank p's finished slice to rank m
+          if (p != m && cnt > 0)
+            CUDA_TRY(cudaMemcpyAsync(pred[m] + (size_t)lo * LE, pred[p] + (size_t)lo * LE, (size_t)cnt * LE * 4, dd, st));
+          break;
+        }
+      }
+    }
+  }
+  return REMOE_OK;
 }
+
+// The multi-rank pipeline for the handles in hs[0..nh) (NCCL: this process's handle;
+// loopback: every rank of the group).  local(h) runs S1-S4 (or the tree search) into
+// h->local_top; then exchange 1, S5-S7 and exchange 2.  ids/scores/pred are per handle.
+template <class LocalStage>
+static remoe_status_t query_ranks(remoe_sps* const* hs, int nh, int bc, int k, int64_t* const* ids,
+                                  float* const* scores, float* const* pred, cudaStream_t st, int* launches,
+                                  LocalStage&& local) {
+  for (int i = 0; i < nh; ++i) ST_TRY(local(hs[i]));
+  ST_TRY(exchange(hs, nh, Xchg::Keys, bc, k, pred, st));
+  const bool want = pred != nullptr && pred[0] != nullptr;
+  for (int i = 0; i < nh; ++i) ST_TRY(stage_merge(hs[i], bc, k, ids[i], scores[i], want, st, launches));
+  if (!want) return REMOE_OK;
+  const bool ag = xchg_allgather(hs[0], bc);
+  ST_TRY(exchange(hs, nh, ag ? Xchg::PartsAllGather : Xchg::PartsAllToAll, bc, k, pred, st));
+  for (int i = 0; i < nh; ++i) ST_TRY(stage_combine(hs[i], bc, pred[i], st, launches));
+  if (!ag) ST_TRY(exchange(hs, nh, Xchg::SlicesBroadcast, bc, k, pred, st));
+  return REMOE_OK;
+}
+
+static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k, int64_t* ids,
+                                  float* scores, float* pred, cudaStream_t st, int* launches) {
+  const remoe_sps_config_t& c = h->cfg;
+  if (c.world == 1) {
+    const remoe::FinalizeArgs fin{h->act, c.global_offset, c.n_local, 0, h->LE, c.temperature, ids, scores, pred};
+    return stage_scan(h, q, bc, k, &fin, st, launches);
+  }
+  remoe_sps* hs[1] = {h};
+  return query_ranks(hs, 1, bc, k, &ids, &scores, &pred, st, launches,
+                     [&](remoe_sps* hh) { return stage_scan(hh, q, bc, k, nullptr, st, launches); });
+}
+
+static bool aligned(const void* p, size_t a) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
 static remoe_status_t check_query(remoe_sps* h, const uint16_t* q, int32_t B, int32_t k,
-                                  const int64_t* ids, const float* scores) {
+                                  const int64_t* ids, const float* scores, const float* pred,
+                                  bool device_bufs = true) {
   if (!h) return fail(REMOE_ERR_STATE, "handle is NULL");
   if (B < 0) return fail(REMOE_ERR_INVALID_ARG, "B must be >= 0");
   if (k < 1) return fail(REMOE_ERR_INVALID_ARG, "k must be >= 1");
@@ -570,17 +853,76 @@ static remoe_status_t check_query(remoe_sps* h, const uint16_t* q, int32_t B, in
     return fail(REMOE_ERR_INVALID_ARG, "k=%d exceeds the history size %lld (SPEC S:227)", k,
                 (long long)h->n_total);
   if (B > 0 && (!q || !ids || !scores)) return fail(REMOE_ERR_INVALID_ARG, "q/ids/scores is NULL");
+  // the kernels read q with 16-byte vector loads / cp.async and write pred with float4 stores
+  if (device_bufs && (!aligned(q, 16) || !aligned(pred, 16) || !aligned(ids, 8) || !aligned(scores, 4)))
+    return fail(REMOE_ERR_INVALID_ARG, "misaligned buffer: q and pred need 16 bytes, ids 8, scores 4");
   return REMOE_OK;
 }
 
+// The device-buffer query of one chunk (world == 1) through a cached CUDA graph: captured
+// once per (buffers, B, k, kernel choice), replayed as one launch on the library stream,
+// ordered after the caller's earlier work and before its later work by two events.
+static remoe_status_t query_device_graph(remoe_sps* h, const uint16_t* q, int B, int k, int64_t* ids,
+                                         float* scores, float* pred, cudaStream_t caller) {
+  if (!h->gst) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->gst, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&h->gev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&h->gev_done, cudaEventDisableTiming));
+  }
+  remoe_sps::DevGraph* g = nullptr;
+  for (auto& e : h->dg)
+    if (e.exec && e.q == q && e.ids == ids && e.scores == scores && e.pred == pred && e.B == B && e.k == k &&
+        e.kernel == h->force_kernel) { g = &e; break; }
+  const cudaStream_t st = h->gst;
+  CUDA_TRY(cudaEventRecord(h->gev, caller));
+  CUDA_TRY(cudaStreamWaitEvent(st, h->gev, 0));
+  if (!g) {
+    g = &h->dg[0];
+    for (auto& e : h->dg)
+      if (e.used < g->used) g = &e;  // least recently used (or empty) slot
+    g->reset();
+    CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    int launches = 0;
+    const remoe_status_t qs = query_chunk(h, q, B, k, ids, scores, pred, st, &launches);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+    if (qs != REMOE_OK || ce != cudaSuccess || !graph) {
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      if (qs != REMOE_OK) return qs;
+      return fail(REMOE_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+    }
+    const cudaError_t ie = cudaGraphInstantiate(&g->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+      g->reset();
+      return fail(REMOE_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ie));
+    }
+    g->q = q; g->ids = ids; g->scores = scores; g->pred = pred;
+    g->B = B; g->k = k; g->kernel = h->force_kernel; g->launches = launches;
+  }
+  g->used = ++h->dg_clock;
+  CUDA_TRY(cudaGraphLaunch(g->exec, st));
+  CUDA_TRY(cudaEventRecord(h->gev_done, st));
+  CUDA_TRY(cudaStreamWaitEvent(caller, h->gev_done, 0));
+  h->last_launches = g->launches;
+  return REMOE_OK;
+}
+
+extern "C" {
+
 remoe_status_t remoe_sps_query(remoe_sps_t h, const uint16_t* q, int32_t B, int32_t k,
                                int64_t* ids, float* scores, float* pred, void* stream) {
-  ST_TRY(check_query(h, q, B, k, ids, scores));
+  ST_TRY(check_query(h, q, B, k, ids, scores, pred));
+  if (h->group) return fail(REMOE_ERR_STATE, "a loopback group member is queried with remoe_sps_query_group");
   if (B == 0) return REMOE_OK;
   DeviceGuard dg(h->cfg.device);
+  NvtxRange nr("remoe_sps_query");
   cudaStream_t st = (cudaStream_t)stream;
-  int launches = 0;
   const int mb = h->cfg.max_batch;
+  if (B <= mb && h->cfg.world == 1 && !h->prof && h->use_graphs)
+    return query_device_graph(h, q, B, k, ids, scores, pred, st);
+  int launches = 0;
   for (int b0 = 0; b0 < B; b0 += mb) {
     const int bc = std::min(mb, B - b0);
     ST_TRY(query_chunk(h, q + (size_t)b0 * h->cfg.dim, bc, k, ids + (size_t)b0 * k,
@@ -588,6 +930,56 @@ remoe_status_t remoe_sps_query(remoe_sps_t h, const uint16_t* q, int32_t B, int3
                        &launches));
   }
   h->last_launches = launches;
+  return REMOE_OK;
+}
+
+// Loopback group query (test harness of the multi-rank path on one device).
+remoe_status_t remoe_sps_query_group(remoe_group_t g, const uint16_t* q, int32_t B, int32_t k,
+                                     int64_t* const* ids, float* const* scores, float* const* pred, void* stream) {
+  if (!g) return fail(REMOE_ERR_STATE, "group is NULL");
+  const int G = g->world;
+  if (!ids || !scores) return fail(REMOE_ERR_INVALID_ARG, "ids/scores arrays are NULL");
+  for (int r = 0; r < G; ++r)
+    if (!g->members[r]) return fail(REMOE_ERR_STATE, "rank %d of the loopback group is not built", r);
+  remoe_sps* const* hs = g->members.data();
+  const int dev = hs[0]->cfg.device;
+  int64_t expect = 0;
+  for (int r = 0; r < G; ++r) {
+    const remoe_sps_config_t& c = hs[r]->cfg;
+    if (c.device != dev) return fail(REMOE_ERR_STATE, "loopback ranks must share one device");
+    if (c.global_offset != expect)
+      return fail(REMOE_ERR_INVALID_ARG, "shards do not tile [0, N): rank %d offset %lld, expected %lld", r,
+                  (long long)c.global_offset, (long long)expect);
+    expect += c.n_local;
+    if (c.dim != hs[0]->cfg.dim || hs[r]->LE != hs[0]->LE || c.max_batch != hs[0]->cfg.max_batch)
+      return fail(REMOE_ERR_INVALID_ARG, "loopback ranks differ in dim, table shape or max_batch");
+  }
+  for (int r = 0; r < G; ++r) hs[r]->n_total = expect;
+  const bool want = pred != nullptr && pred[0] != nullptr;
+  for (int r = 0; r < G; ++r) {
+    ST_TRY(check_query(hs[r], q, B, k, ids[r], scores[r], want ? pred[r] : nullptr));
+    if (want && !pred[r]) return fail(REMOE_ERR_INVALID_ARG, "pred must be given for every rank or none");
+  }
+  if (B == 0) return REMOE_OK;
+  DeviceGuard dgd(dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int mb = hs[0]->cfg.max_batch;
+  const int64_t LE = hs[0]->LE;
+  int launches = 0;
+  std::vector<int64_t*> ic(G);
+  std::vector<float*> sc(G), pc(G);
+  for (int b0 = 0; b0 < B; b0 += mb) {
+    const int bc = std::min(mb, B - b0);
+    for (int r = 0; r < G; ++r) {
+      ic[r] = ids[r] + (size_t)b0 * k;
+      sc[r] = scores[r] + (size_t)b0 * k;
+      pc[r] = want ? pred[r] + (size_t)b0 * LE : nullptr;
+    }
+    const uint16_t* qc = q + (size_t)b0 * hs[0]->cfg.dim;
+    ST_TRY(query_ranks(hs, G, bc, k, ic.data(), sc.data(), want ? pc.data() : nullptr, st, &launches,
+                       [&](remoe_sps* hh) { return stage_scan(hh, qc, bc, k, nullptr, st, &launches); }));
+  }
+  for (int r = 0; r < G; ++r) hs[r]->last_launches = launches;
   return REMOE_OK;
 }
 
@@ -611,6 +1003,7 @@ static remoe_status_t query_host_graph(remoe_sps* h, const uint16_t* q, int B, i
   if (!h->gst) {
     CUDA_TRY(cudaStreamCreateWithFlags(&h->gst, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&h->gev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&h->gev_done, cudaEventDisableTiming));
   }
   st = h->gst;
   CUDA_TRY(cudaEventRecord(h->gev, caller));  // after the caller's earlier work on the handle
@@ -668,14 +1061,17 @@ static remoe_status_t query_host_graph(remoe_sps* h, const uint16_t* q, int B, i
 
 remoe_status_t remoe_sps_query_host(remoe_sps_t h, const uint16_t* q, int32_t B, int32_t k,
                                     int64_t* ids, float* scores, float* pred, void* stream) {
-  ST_TRY(check_query(h, q, B, k, ids, scores));
+  if (!h) return fail(REMOE_ERR_STATE, "handle is NULL");
+  ST_TRY(check_query(h, q, B, k, ids, scores, pred, false));  // host buffers: staged, any alignment
+  if (h->group) return fail(REMOE_ERR_STATE, "a loopback group member is queried with remoe_sps_query_group");
   if (B == 0) return REMOE_OK;
   DeviceGuard dg(h->cfg.device);
+  NvtxRange nr("remoe_sps_query_host");
   cudaStream_t st = (cudaStream_t)stream;
   const int mb = h->cfg.max_batch;
   const int D = h->cfg.dim;
   int launches = 0;
-  if (B <= mb && h->cfg.world == 1 && !h->prof && !getenv("REMOE_NO_GRAPH")) {
+  if (B <= mb && h->cfg.world == 1 && !h->prof && h->use_graphs) {
     remoe_status_t gs = query_host_graph(h, q, B, k, ids, scores, pred, st);
     if (gs != REMOE_ERR_UNSUPPORTED) return gs;  // UNSUPPORTED: pageable buffers -> direct path
   }
@@ -754,10 +1150,12 @@ remoe_status_t remoe_sps_tree_export(remoe_sps_t h, int64_t* perm, int64_t* begi
 
 remoe_status_t remoe_sps_tree_query(remoe_sps_t h, const uint16_t* q, int32_t B, int32_t k, int64_t* ids,
                                     float* scores, float* pred, int32_t* leaf, int32_t* n_eval, void* stream) {
-  ST_TRY(check_query(h, q, B, k, ids, scores));
+  ST_TRY(check_query(h, q, B, k, ids, scores, pred));
   if (!h->has_tree) return fail(REMOE_ERR_STATE, "no tree: call remoe_sps_tree_build first");
+  if (h->group) return fail(REMOE_ERR_UNSUPPORTED, "tree queries over a loopback group");
   if (B == 0) return REMOE_OK;
   DeviceGuard dg(h->cfg.device);
+  NvtxRange nr("remoe_sps_tree_query");
   cudaStream_t st = (cudaStream_t)stream;
   const remoe_sps_config_t& c = h->cfg;
   const int mb = c.max_batch;
@@ -765,13 +1163,26 @@ remoe_status_t remoe_sps_tree_query(remoe_sps_t h, const uint16_t* q, int32_t B,
   for (int b0 = 0; b0 < B; b0 += mb) {
     const int bc = std::min(mb, B - b0);
     const uint16_t* qc = q + (size_t)b0 * c.dim;
-    CUDA_TRY(remoe::launch_norms(qc, bc, c.dim, h->qnorm, st));
-    CUDA_TRY(remoe::launch_tree_search(h->tree, h->x, h->xnorm, c.dim, qc, h->qnorm, bc, k, c.sigma,
-                                       c.global_offset, h->local_top, leaf ? leaf + b0 : nullptr,
-                                       n_eval ? n_eval + b0 : nullptr, st));
-    launches += 2;
-    ST_TRY(post_local_top(h, bc, k, ids + (size_t)b0 * k, scores + (size_t)b0 * k,
-                          pred ? pred + (size_t)b0 * h->LE : nullptr, st, &launches));
+    int64_t* ic = ids + (size_t)b0 * k;
+    float* sc = scores + (size_t)b0 * k;
+    float* pc = pred ? pred + (size_t)b0 * h->LE : nullptr;
+    auto local = [&](remoe_sps* hh) -> remoe_status_t {
+      CUDA_TRY(remoe::launch_norms(qc, bc, c.dim, hh->qnorm, st));
+      CUDA_TRY(remoe::launch_tree_search(hh->tree, hh->x, hh->xnorm, c.dim, qc, hh->qnorm, bc, k, c.sigma,
+                                         c.global_offset, hh->local_top, leaf ? leaf + b0 : nullptr,
+                                         n_eval ? n_eval + b0 : nullptr, st));
+      launches += 2;
+      return REMOE_OK;
+    };
+    if (c.world == 1) {
+      ST_TRY(local(h));
+      const remoe::FinalizeArgs f{h->act, c.global_offset, c.n_local, 0, h->LE, c.temperature, ic, sc, pc};
+      CUDA_TRY(remoe::launch_finalize(h->local_top, bc, k, f, st));
+      ++launches;
+    } else {
+      remoe_sps* hs[1] = {h};
+      ST_TRY(query_ranks(hs, 1, bc, k, &ic, &sc, &pc, st, &launches, local));
+    }
   }
   h->last_launches = launches;
   return REMOE_OK;

@@ -20,20 +20,42 @@ constexpr int kSeedMinB = 32;
 constexpr int64_t kSeedSmallRows = 512 * 1024;
 constexpr int kSeedMinBSmall = 8;
 constexpr int kSeedStride = 64;
-// L2 promotion of the store's TMA boxes (128 B per row per box); REMOE_TC_PROMO = 0 none,
-// 1 64 B, 2 128 B, 3 256 B.
-inline CUtensorMapL2promotion tmap_promotion() {
-  const char* e = getenv("REMOE_TC_PROMO");
-  const int v = e ? atoi(e) : 3;
-  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-       : v == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-       : v == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-}
-// K-block visiting order of the tensor-core scans (tcgen05.cuh kb_at); REMOE_TC_KB_ORDER.
-inline int kb_order_env() {
-  const char* e = getenv("REMOE_TC_KB_ORDER");
-  return e ? atoi(e) : 0;
-}
+// Experiment / debug knobs of the tensor-core scans, read from the environment ONCE when a
+// plan is created (remoe_sps_build), never on the launch path.
+struct TcKnobs {
+  int promo = 3;             // REMOE_TC_PROMO: L2 promotion of TMA boxes (0 none, 1 64 B, 2 128 B, 3 256 B)
+  int kb_order = 0;          // REMOE_TC_KB_ORDER: K-block visiting order (tcgen05.cuh kb_at)
+  bool full_slab = false;    // REMOE_TC_FULL_SLAB: always store M query rows per K-block
+  bool global_bufs = false;  // REMOE_TC_GLOBAL_BUFS: LaneTopk buffers in global memory
+  int stages = 0;            // REMOE_TC_STAGES: cap the stage ring (0: as many as fit)
+  bool no_multicast = false; // REMOE_NO_MULTICAST: no cluster multicast of store tiles
+  int epi_sleep = 0;         // REMOE_EPI_SLEEP: epilogue waits with a suspend-time hint
+  int dbg = 0;               // REMOE_TC_DBG: experiment bits (wrong results)
+  bool stats = false;        // REMOE_TC_STATS: candidate / insert counters (prints, syncs)
+  bool trace = false;        // REMOE_TC_TRACE: per-CTA phase stamps (prints, syncs)
+  bool verbose = false;      // REMOE_VERBOSE
+  static TcKnobs from_env() {
+    TcKnobs k;
+    auto ival = [](const char* n, int d) { const char* e = getenv(n); return e ? atoi(e) : d; };
+    k.promo = ival("REMOE_TC_PROMO", 3);
+    k.kb_order = ival("REMOE_TC_KB_ORDER", 0);
+    k.full_slab = getenv("REMOE_TC_FULL_SLAB") != nullptr;
+    k.global_bufs = getenv("REMOE_TC_GLOBAL_BUFS") != nullptr;
+    k.stages = ival("REMOE_TC_STAGES", 0);
+    k.no_multicast = getenv("REMOE_NO_MULTICAST") != nullptr;
+    k.epi_sleep = ival("REMOE_EPI_SLEEP", 0);
+    k.dbg = ival("REMOE_TC_DBG", 0);
+    k.stats = getenv("REMOE_TC_STATS") != nullptr;
+    k.trace = getenv("REMOE_TC_TRACE") != nullptr;
+    k.verbose = getenv("REMOE_VERBOSE") != nullptr;
+    return k;
+  }
+  CUtensorMapL2promotion promotion() const {
+    return promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+         : promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+         : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+};
 inline int seed_ks_for(int k) { return k <= 32 ? 1 : k <= 64 ? 2 : 4; }
 
 struct TcPlan {
@@ -49,6 +71,10 @@ struct TcPlan {
   // Tiled copy of the store (tc_tile_store), or nullptr: box (tile, kb) = 128 rows x 64
   // elements, pre-swizzled (SWIZZLE_128B) and contiguous, 16 KB at xt + (tile*nkb + kb)*8192.
   const uint16_t* xt = nullptr;
+  TcKnobs kn;                 // read once at plan creation
+  // debug buffers of this plan (REMOE_TC_STATS / REMOE_TC_TRACE), freed by tc_plan_destroy
+  unsigned long long* stats_buf = nullptr;
+  unsigned long long* trace_buf = nullptr;
 };
 
 // Writes the tiled, pre-swizzled copy of x [n_rows x dim] (dim % 64 == 0) into xt

@@ -15,10 +15,12 @@ from .sps import Sps, remoe_nccl_unique_id
 
 
 def shard_range(n_total: int, world: int, rank: int) -> tuple[int, int]:
-    """Contiguous row shard of `rank`: (global offset, rows).  Ranks tile [0, n_total)."""
-    per = -(-n_total // world)
-    lo = min(n_total, rank * per)
-    hi = min(n_total, lo + per)
+    """Contiguous row shard of `rank`: (global offset, rows), the balanced split
+    offset_g = floor(n_total * g / world).  Ranks tile [0, n_total); every shard is
+    non-empty whenever n_total >= world (a ceil(n/world) split can leave the last ranks
+    empty, e.g. n = 9 over 4 ranks)."""
+    lo = n_total * rank // world
+    hi = n_total * (rank + 1) // world
     return lo, hi - lo
 
 

@@ -26,6 +26,7 @@ ABI_FUNCTIONS = (
     "remoe_sps_set_kernel", "remoe_sps_profile", "remoe_sps_destroy", "remoe_status_string",
     "remoe_last_error", "remoe_sps_embed", "remoe_js_divergence",
     "remoe_sps_tree_build", "remoe_sps_tree_info", "remoe_sps_tree_export", "remoe_sps_tree_query",
+    "remoe_loopback_group_create", "remoe_loopback_group_destroy", "remoe_sps_query_group",
 )
 
 
@@ -64,6 +65,7 @@ class SpsConfig(ctypes.Structure):
         ("nccl_unique_id", ctypes.c_void_p),
         ("inputs_on_device", ctypes.c_int32),
         ("validate", ctypes.c_int32),
+        ("loopback_group", ctypes.c_void_p),
     ]
 
 
@@ -114,6 +116,9 @@ def lib():
         L.remoe_sps_tree_info.argtypes = [vp, ctypes.POINTER(TreeInfo)]
         L.remoe_sps_tree_export.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp]
         L.remoe_sps_tree_query.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp]
+        L.remoe_loopback_group_create.argtypes = [i32, ctypes.POINTER(vp)]
+        L.remoe_loopback_group_destroy.argtypes = [vp]
+        L.remoe_sps_query_group.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp]
         L.remoe_sps_destroy.argtypes = [vp]
         L.remoe_sps_destroy.restype = None
         L.remoe_status_string.argtypes = [i32]
@@ -124,7 +129,8 @@ def lib():
                   "remoe_nccl_unique_id", "remoe_sps_sync", "remoe_sps_get_info",
                   "remoe_sps_set_kernel", "remoe_sps_profile", "remoe_sps_embed",
                   "remoe_js_divergence", "remoe_sps_tree_build", "remoe_sps_tree_info",
-                  "remoe_sps_tree_export", "remoe_sps_tree_query"):
+                  "remoe_sps_tree_export", "remoe_sps_tree_query", "remoe_loopback_group_create",
+                  "remoe_loopback_group_destroy", "remoe_sps_query_group"):
             getattr(L, f).restype = i32
         _LIB = L
     return _LIB
@@ -146,11 +152,13 @@ def _ptr(t) -> int | None:
     return t.data_ptr()
 
 
-def _stream(stream) -> int | None:
+def _stream(stream, device=None) -> int | None:
+    """The stream to enqueue on: the given one, else torch's current stream of `device`
+    (the handle's device -- not the current device, which may be another GPU)."""
     if stream is not None:
         return int(stream) if isinstance(stream, int) else stream.cuda_stream
     import torch
-    return torch.cuda.current_stream().cuda_stream
+    return torch.cuda.current_stream(device).cuda_stream
 
 
 # ------------------------------------------------------------------ C-ABI-named calls
@@ -179,21 +187,47 @@ def remoe_sps_build(cfg: SpsConfig, emb_bf16, act, nccl_unique_id: bytes | None 
     return h.value
 
 
+def _dev(t):
+    return t.device if getattr(t, "is_cuda", False) else None
+
+
 def remoe_sps_query(h: int, q_bf16, B: int, k: int, ids, scores, pred=None, stream=None):
     """S1-S7 on device buffers (torch CUDA tensors)."""
     _check(lib().remoe_sps_query(h, _ptr(q_bf16), B, k, _ptr(ids), _ptr(scores), _ptr(pred),
-                                 _stream(stream)))
+                                 _stream(stream, _dev(ids))))
 
 
-def remoe_sps_query_host(h: int, q_bf16, B: int, k: int, ids, scores, pred=None, stream=None):
+def remoe_loopback_group_create(world: int) -> int:
+    """An empty loopback group of `world` ranks (one process, one device; test harness of
+    the multi-rank exchange, include/remoe.h)."""
+    g = ctypes.c_void_p()
+    _check(lib().remoe_loopback_group_create(world, ctypes.byref(g)))
+    return g.value
+
+
+def remoe_loopback_group_destroy(g: int):
+    _check(lib().remoe_loopback_group_destroy(g))
+
+
+def remoe_sps_query_group(g: int, q_bf16, B: int, k: int, ids, scores, pred=None, stream=None):
+    """remoe_sps_query for every rank of a loopback group: ids/scores/pred are lists with
+    one device tensor per rank (pred None: S6-S7 skipped)."""
+    n = len(ids)
+    arr = lambda ts: (ctypes.c_void_p * n)(*[_ptr(t) for t in ts])  # noqa: E731
+    _check(lib().remoe_sps_query_group(g, _ptr(q_bf16), B, k, arr(ids), arr(scores),
+                                       arr(pred) if pred is not None else None,
+                                       _stream(stream, _dev(ids[0]))))
+
+
+def remoe_sps_query_host(h: int, q_bf16, B: int, k: int, ids, scores, pred=None, stream=None, device=None):
     """S1-S7 on host buffers (numpy or pinned CPU tensors); synchronous."""
     _check(lib().remoe_sps_query_host(h, _ptr(q_bf16), B, k, _ptr(ids), _ptr(scores), _ptr(pred),
-                                      _stream(stream)))
+                                      _stream(stream, device)))
 
 
 def remoe_expert_plan(pred, B: int, L: int, E: int, n_cold: int, cold_mask, stream=None):
     """S8 on device buffers."""
-    _check(lib().remoe_expert_plan(_ptr(pred), B, L, E, n_cold, _ptr(cold_mask), _stream(stream)))
+    _check(lib().remoe_expert_plan(_ptr(pred), B, L, E, n_cold, _ptr(cold_mask), _stream(stream, _dev(pred))))
 
 
 def remoe_sps_sync(h: int):
@@ -222,7 +256,7 @@ def remoe_sps_embed(tokens_bf16, offsets, n_prompts: int, dim: int, out_bf16=Non
                     stream=None):
     """NEXT-N1: prompt vectors a_p = sum_t x_t / |x_t| from token embeddings (device buffers)."""
     _check(lib().remoe_sps_embed(_ptr(tokens_bf16), _ptr(offsets), n_prompts, dim, _ptr(out_bf16),
-                                 _ptr(out_f32), _stream(stream)))
+                                 _ptr(out_f32), _stream(stream, _dev(tokens_bf16))))
 
 
 def embed(tokens_bf16, offsets, want_f32=False, stream=None):
@@ -240,7 +274,7 @@ def embed(tokens_bf16, offsets, want_f32=False, stream=None):
 def remoe_js_divergence(P, Q, shared_q: bool, B: int, L: int, E: int, out, stream=None):
     """NEXT-N4: out[b] = mean_l JS_2(P[b,l], Q[b,l] or Q[l]) on device buffers."""
     _check(lib().remoe_js_divergence(_ptr(P), _ptr(Q), 1 if shared_q else 0, B, L, E, _ptr(out),
-                                     _stream(stream)))
+                                     _stream(stream, _dev(P))))
 
 
 def js_divergence(P, Q, stream=None):
@@ -278,7 +312,7 @@ def remoe_sps_tree_query(h: int, q_bf16, B: int, k: int, ids, scores, pred=None,
                          stream=None):
     """NEXT-N2: Algorithm 1 + S6/S7 on device buffers."""
     _check(lib().remoe_sps_tree_query(h, _ptr(q_bf16), B, k, _ptr(ids), _ptr(scores), _ptr(pred), _ptr(leaf),
-                                      _ptr(n_eval), _stream(stream)))
+                                      _ptr(n_eval), _stream(stream, _dev(ids))))
 
 
 def remoe_sps_destroy(h: int):
@@ -292,7 +326,8 @@ class Sps:
     """Owns one handle.  Tensors in, tensors out (torch on the handle's device)."""
 
     def __init__(self, emb_bf16, act, *, sigma=1e-6, temperature=1.0, max_batch=256, max_k=128,
-                 device=0, rank=0, world=1, global_offset=0, nccl_unique_id=None, validate=True):
+                 device=0, rank=0, world=1, global_offset=0, nccl_unique_id=None, validate=True,
+                 loopback_group=None):
         import torch
         cfg = remoe_sps_config_default()
         n, d = emb_bf16.shape
@@ -302,6 +337,7 @@ class Sps:
         cfg.max_batch, cfg.max_k = max_batch, max_k
         cfg.device, cfg.rank, cfg.world = device, rank, world
         cfg.validate = 1 if validate else 0
+        cfg.loopback_group = loopback_group
         on_dev = isinstance(emb_bf16, torch.Tensor) and emb_bf16.is_cuda
         cfg.inputs_on_device = 1 if on_dev else 0
         self.device = torch.device("cuda", device)
@@ -324,7 +360,7 @@ class Sps:
         ids = np.empty((B, k), np.int64)
         scores = np.empty((B, k), np.float32)
         pred = np.empty((B, self.layers, self.experts), np.float32) if want_pred else None
-        remoe_sps_query_host(self.handle, q_bf16, B, k, ids, scores, pred, stream)
+        remoe_sps_query_host(self.handle, q_bf16, B, k, ids, scores, pred, stream, self.device)
         return ids, scores, pred
 
     def tree_build(self, beta=150, branching=8, max_iter=10, seed=0):
@@ -374,6 +410,54 @@ class Sps:
         if getattr(self, "handle", None):
             remoe_sps_destroy(self.handle)
             self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class LoopbackGroup:
+    """G ranks of one row-sharded store in ONE process on ONE device: the multi-rank path
+    (key all-gather + merge, owner-side partial prediction, partial exchange) with device
+    copies in place of NCCL (include/remoe.h "Loopback groups")."""
+
+    def __init__(self, shards, acts, n_total: int, *, device=0, **kw):
+        from .dist import shard_range
+        self.world = len(shards)
+        self.group = remoe_loopback_group_create(self.world)
+        self.ranks = []
+        try:
+            for r, (x, a) in enumerate(zip(shards, acts)):
+                off, n = shard_range(n_total, self.world, r)
+                assert x.shape[0] == n, f"rank {r}: expected {n} rows, got {x.shape[0]}"
+                self.ranks.append(Sps(x, a, device=device, rank=r, world=self.world, global_offset=off,
+                                      loopback_group=self.group, **kw))
+        except Exception:
+            self.close()
+            raise
+        s0 = self.ranks[0]
+        self.device, self.layers, self.experts = s0.device, s0.layers, s0.experts
+
+    def query(self, q_bf16, k, want_pred=True, stream=None):
+        """Every rank's (ids, scores, pred) as lists of device tensors (identical values)."""
+        import torch
+        B = q_bf16.shape[0]
+        ids = [torch.empty((B, k), dtype=torch.int64, device=self.device) for _ in range(self.world)]
+        scores = [torch.empty((B, k), dtype=torch.float32, device=self.device) for _ in range(self.world)]
+        pred = ([torch.empty((B, self.layers, self.experts), dtype=torch.float32, device=self.device)
+                 for _ in range(self.world)] if want_pred else None)
+        remoe_sps_query_group(self.group, q_bf16, B, k, ids, scores, pred, stream)
+        return ids, scores, pred
+
+    def close(self):
+        for s in getattr(self, "ranks", []):
+            s.close()
+        self.ranks = []
+        if getattr(self, "group", None):
+            remoe_loopback_group_destroy(self.group)
+            self.group = None
 
     def __del__(self):
         try:

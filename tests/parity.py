@@ -1,8 +1,14 @@
 """The GPU-vs-oracle parity protocol (SURVEY.md §8(c) 'Parity protocol').
 
 * ids: the GPU set may differ from the oracle set only by ids whose oracle score
-  is within `tol` of the oracle's k-th score; positions may swap only between ids
-  whose oracle scores are within `tol` of each other.
+  is within `tol` (BASELINE 1e-4) AND within the tight window `tight` (1e-5) of the
+  oracle's k-th score; positions may swap only between ids whose oracle scores are
+  within `tight` of each other.  The tight window is SURVEY §8(c)'s internal check: a
+  1e-4 window alone would pass a top-k that returns the (k+1)-th row instead of the
+  k-th on about half of the clustered queries, while a genuine fp32 rounding swap needs
+  a gap of ~2e-6.  Every run counts the substitutions (`substitutions`) and the
+  oracle-only boundary near-tie rate (`boundary_ties`: queries where another row lies
+  within `tol` of the k-th score).
 * scores: each GPU score vs the ORACLE score of the same id, |d| <= tol, and the
   internal tight window |d| <= tight.
 * pred: vs the oracle prediction (re-derived on the GPU's id set, with oracle
@@ -26,12 +32,18 @@ TIGHT = 1e-5
 class ParityReport:
     queries: int = 0
     substitutions: int = 0
+    boundary_ties: int = 0
     max_score_err: float = 0.0
     max_pred_err: float = 0.0
     failures: list = field(default_factory=list)
 
     def ok(self):
         return not self.failures
+
+    def summary(self):
+        return (f"{self.queries} queries: {self.substitutions} near-tie substitutions, "
+                f"{self.boundary_ties} oracle boundary near-ties (1e-4), "
+                f"max |dscore| {self.max_score_err:.2e}, max |dpred| {self.max_pred_err:.2e}")
 
 
 def compare(q_bits, x_bits, act, k, gpu_ids, gpu_scores, gpu_pred=None, *, sigma=oracle.SIGMA,
@@ -41,10 +53,20 @@ def compare(q_bits, x_bits, act, k, gpu_ids, gpu_scores, gpu_pred=None, *, sigma
     gpu_scores = np.asarray(gpu_scores, np.float64)
     B = q_bits.shape[0]
     if oracle_out is None:
-        oracle_out = oracle.sps(q_bits, x_bits, act, k, sigma=sigma, id_offset=id_offset,
-                                want_pred=gpu_pred is not None)
+        # one extra column (k + 1) gives the boundary near-tie rate for free
+        kk = k + 1 if k < x_bits.shape[0] else k
+        oracle_out = oracle.sps(q_bits, x_bits, act, kk, sigma=sigma, id_offset=id_offset,
+                                want_pred=False)
+        o_pred = None
+        if gpu_pred is not None:
+            o_pred = np.stack([oracle.predict(oracle_out[0][i, :k], oracle.softmax(oracle_out[1][i, :k]),
+                                              act, id_offset=id_offset) for i in range(B)])
+        oracle_out = (oracle_out[0], oracle_out[1], o_pred)
     o_ids, o_sc, o_pred = oracle_out
     rep = ParityReport(queries=B)
+    if o_ids.shape[1] == k + 1:  # oracle run with k + 1: the (k+1)-th score is known
+        rep.boundary_ties = int(np.sum(np.abs(o_sc[:, k] - o_sc[:, k - 1]) <= tol))
+        o_ids, o_sc = o_ids[:, :k], o_sc[:, :k]
     qi = np.repeat(np.arange(B), k)
     rows = gpu_ids.reshape(-1) - id_offset
     if rows.min() < 0 or rows.max() >= x_bits.shape[0]:
@@ -63,17 +85,19 @@ def compare(q_bits, x_bits, act, k, gpu_ids, gpu_scores, gpu_pred=None, *, sigma
             rep.substitutions += len(extra)
             if exact_ids:
                 rep.failures.append(f"q{i}: id sets differ (exact required): +{extra} -{missing}")
+            win = min(tol, tight)
             for r in range(k):
-                if gpu_ids[i, r] in extra and abs(s_of_gpu[i, r] - sk) > tol:
+                if gpu_ids[i, r] in extra and abs(s_of_gpu[i, r] - sk) > win:
                     rep.failures.append(f"q{i}: GPU id {gpu_ids[i, r]} (oracle score {s_of_gpu[i, r]:.8f})"
-                                        f" not within {tol} of the k-th score {sk:.8f}")
+                                        f" not within {win} of the k-th score {sk:.8f}")
             for r in range(k):
-                if o_ids[i, r] in missing and abs(o_sc[i, r] - sk) > tol:
-                    rep.failures.append(f"q{i}: oracle id {o_ids[i, r]} missing and not a near tie")
-        # order: any inversion (by oracle score) must be a near tie
+                if o_ids[i, r] in missing and abs(o_sc[i, r] - sk) > win:
+                    rep.failures.append(f"q{i}: oracle id {o_ids[i, r]} missing and not a near tie"
+                                        f" (within {win})")
+        # order: any inversion (by oracle score) must be a near tie (tight window)
         for r in range(k - 1):
-            if s_of_gpu[i, r] < s_of_gpu[i, r + 1] - tol:
-                rep.failures.append(f"q{i}: order inversion at {r} beyond tol")
+            if s_of_gpu[i, r] < s_of_gpu[i, r + 1] - min(tol, tight):
+                rep.failures.append(f"q{i}: order inversion at {r} beyond {min(tol, tight)}")
         # the GPU's own list must be sorted by its own key (score desc, id asc)
         for r in range(k - 1):
             a, b = gpu_scores[i, r], gpu_scores[i, r + 1]
@@ -96,6 +120,36 @@ def compare(q_bits, x_bits, act, k, gpu_ids, gpu_scores, gpu_pred=None, *, sigma
             if perr > tol:
                 rep.failures.append(f"q{i}: pred error {perr:.3e} > {tol}")
     return rep
+
+
+def oracle_run(q_bits, x_bits, act, k, *, sigma=oracle.SIGMA, id_offset=0, want_pred=True):
+    """The oracle's top-(k+1) (for the boundary near-tie count) with the prediction of its
+    top-k: the tuple `compare(..., oracle_out=...)` takes."""
+    kk = k + 1 if k < x_bits.shape[0] else k
+    ids, sc, _ = oracle.sps(q_bits, x_bits, act, kk, sigma=sigma, id_offset=id_offset, want_pred=False)
+    pred = None
+    if want_pred:
+        pred = np.stack([oracle.predict(ids[i, :k], oracle.softmax(sc[i, :k]), act, id_offset=id_offset)
+                         for i in range(q_bits.shape[0])])
+    return ids, sc, pred
+
+
+def take(oracle_out, rows):
+    """Rows of an oracle_run result (pred may be None)."""
+    return tuple(None if v is None else v[rows] for v in oracle_out)
+
+
+def log_report(name, rep):
+    """Append one parity report line to $REMOE_PARITY_LOG (GPU runs keep it under profiles/)."""
+    import json
+    import os
+    print(f"[parity] {name}: {rep.summary()}")
+    path = os.environ.get("REMOE_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps({"test": name, "queries": rep.queries, "substitutions": rep.substitutions,
+                                "boundary_ties_1e-4": rep.boundary_ties, "max_score_err": rep.max_score_err,
+                                "max_pred_err": rep.max_pred_err, "ok": rep.ok()}) + "\n")
 
 
 def plan_compare(pred_oracle, gpu_mask, n_cold, tol=TOL):

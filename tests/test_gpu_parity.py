@@ -9,7 +9,7 @@ import pytest
 
 import gen
 import oracle
-from parity import compare, plan_compare
+from parity import compare, log_report, oracle_run, plan_compare, take
 
 torch = pytest.importorskip("torch")
 pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("remoe_lib_built")]
@@ -59,7 +59,9 @@ def kernel_available(sps, which):
         return False
 
 
-def assert_parity(rep):
+def assert_parity(rep, name=None):
+    if name:
+        log_report(name, rep)
     assert rep.ok(), "\n".join(rep.failures[:20])
 
 
@@ -95,7 +97,7 @@ def c2_oracle(B, k):
     key = (B, k)
     if key not in _C2Q:
         q = gen.queries(c.store_seed, c.query_seed, c.n, c.dim, B, mode=1)
-        _C2Q[key] = (q, oracle.sps(q, x, a, k))
+        _C2Q[key] = (q, oracle_run(q, x, a, k))
     return _C2Q[key]
 
 
@@ -105,7 +107,7 @@ def test_c2_batch_sweep(kern, B):
     c, x, a = store("c2")
     q_all, o_all = c2_oracle(256, c.k)
     q = q_all[:B]
-    o = tuple(v[:B] for v in o_all)
+    o = take(o_all, slice(0, B))
     s = make(x, a, max_k=64)
     if not kernel_available(s, kern):
         pytest.skip(f"{kern} kernel unavailable")
@@ -113,7 +115,7 @@ def test_c2_batch_sweep(kern, B):
         pytest.skip("streaming kernel is only used for small batches")
     ids, sc, pred = run(s, q, c.k)
     rep = compare(q, x, a, c.k, ids, sc, pred, oracle_out=o)
-    assert_parity(rep)
+    assert_parity(rep, f"c2 B={B} {kern}")
     assert rep.substitutions == 0, "c2 is well separated at k=10: ids must match exactly"
 
 
@@ -127,7 +129,7 @@ def test_c2_k_sweep(kern, k):
         pytest.skip(f"{kern} kernel unavailable")
     ids, sc, pred = run(s, q, k)
     rep = compare(q, x, a, k, ids, sc, pred)
-    assert_parity(rep)
+    assert_parity(rep, f"c2[20k] k={k} {kern}")
 
 
 # ------------------------------------------------------------------ invariants
@@ -304,52 +306,88 @@ def test_expert_plan_vs_oracle():
 
 # ------------------------------------------------------------------ full-size sampled parity
 
-@pytest.mark.parametrize("kern", ["stream", "tc", "pair"])
-def test_c3_full_size_sampled(kern):
-    """BASELINE c3 (1M x 1024, 24x60, k=16) at its bench batch B=64 (and B=4 for the
-    streaming kernel); 6 sampled queries checked against the oracle one by one."""
+_C3O = {}
+
+
+def c3_oracle(B, k):
+    """The oracle on the c3 bench batch (fresh cluster members, mode 0 as bench.py times it)
+    and on the correctness mix (mode 1)."""
     c, x, a = store("c3")
-    B = 64 if kern == "tc" else 4
-    q = gen.queries(c.store_seed, c.query_seed, c.n, c.dim, B, mode=1)
+    key = (B, k)
+    if key not in _C3O:
+        q = gen.queries(c.store_seed, c.query_seed, c.n, c.dim, B, mode=0)
+        _C3O[key] = (q, oracle_run(q, x, a, k))
+    return _C3O[key]
+
+
+@pytest.mark.parametrize("kern", ["tc", "stream", "pair"])
+def test_c3_full_size_bench_batch(kern):
+    """BASELINE c3 (1M x 1024, 24x60, k = 16) at bench.py's batch (B = 64 fresh cluster
+    members, the launch configuration bench.py times): ALL 64 queries against the oracle
+    (tensor-core and CTA-pair scans; the streaming kernel on 8 of them)."""
+    c, x, a = store("c3")
+    q, o = c3_oracle(64, c.k)
+    B = 64 if kern != "stream" else 8
     s = make(x, a, max_k=c.k, max_batch=256)
     if not kernel_available(s, kern):
         pytest.skip(f"{kern} kernel unavailable")
+    ids, sc, pred = run(s, q[:B], c.k)
+    rep = compare(q[:B], x, a, c.k, ids, sc, pred, oracle_out=take(o, slice(0, B)))
+    assert_parity(rep, f"c3 B={B} {kern} (bench batch, all queries)")
+    s.close()
+
+
+def test_c3_full_size_mixed_queries():
+    """c3 with the correctness query mix (fresh, exact copies, perturbed copies,
+    duplicates) at B = 64: 16 sampled queries; copies retrieve their source."""
+    c, x, a = store("c3")
+    B = 64
+    q = gen.queries(c.store_seed, c.query_seed, c.n, c.dim, B, mode=1)
+    s = make(x, a, max_k=c.k, max_batch=256)
     ids, sc, pred = run(s, q, c.k)
-    pick = sorted({0, 1, 3, min(B - 1, 4), min(B - 1, 6), B - 1})
+    pick = list(range(0, 64, 4))
     rep = compare(q[pick], x, a, c.k, ids[pick], sc[pick], pred[pick])
-    assert_parity(rep)
+    assert_parity(rep, "c3 B=64 tc (mixed queries, 16 sampled)")
+    for i in range(B):
+        if i % 8 in (4, 5):
+            assert ids[i, 0] == gen.query_source_row(c.query_seed, c.n, i)
+        if i % 8 == 7:
+            assert np.array_equal(ids[i], ids[i - 1]) and np.array_equal(pred[i], pred[i - 1])
+    s.close()
 
 
 # ------------------------------------------------------------------ BASELINE c4 and c5 (sampled)
 
 def test_c4_full_size_sampled():
     """BASELINE c4: 10M x 1024, Mixtral 32x8 table, k = 32, at B = 1 (single-query latency)
-    and B = 1024 (throughput), on one GPU; sampled queries checked against the oracle."""
+    and B = 1024 (throughput), on one GPU; 1 + 4 sampled queries checked against the oracle."""
     c = gen.CONFIGS["c4"]
     x = gen.store_emb(c.store_seed, c.n, c.dim)
     a = gen.store_act(c.store_seed, c.n, c.layers, c.experts, c.moe_topk)
     q = gen.queries(c.store_seed, c.query_seed, c.n, c.dim, 1024, mode=1)
     s = make(x, a, max_k=32, max_batch=1024)
-    for B, pick in ((1, [0]), (1024, [4, 517, 1023])):
+    for B, pick in ((1, [0]), (1024, [4, 517, 770, 1023])):
         ids, sc, pred = run(s, q[:B], 32)
         rep = compare(q[pick], x, a, 32, ids[pick], sc[pick], pred[pick])
-        assert_parity(rep)
+        assert_parity(rep, f"c4 B={B} ({len(pick)} sampled)")
     s.close()
 
 
 @pytest.mark.parametrize("k", [1, 64, 128])
 def test_c5_sweep_corners_sampled(k):
     """BASELINE c5 corners on the c3 store: B = 4096 (internal chunks of max_batch) and
-    k in {1, 64, 128}; sampled queries vs the oracle."""
+    k in {1, 64, 128}; 16 sampled queries per corner (spread over the 4 chunks) vs the oracle."""
     c, x, a = store("c3")
     q = gen.queries(c.store_seed, c.query_seed, c.n, c.dim, 4096, mode=1)
     s = make(x, a, max_k=128, max_batch=1024)
     ids, sc, pred = run(s, q, k)
-    pick = [0, 5, 2047, 4095]
-    assert_parity(compare(q[pick], x, a, k, ids[pick], sc[pick], pred[pick]))
+    pick = [0, 5, 255, 256, 511, 1023, 1024, 1500, 2047, 2048, 2600, 3071, 3072, 3500, 4094, 4095]
+    assert_parity(compare(q[pick], x, a, k, ids[pick], sc[pick], pred[pick]),
+                  f"c5 B=4096 k={k} (16 sampled)")
     # identical queries (i % 8 == 7 duplicates i - 1) across chunk boundaries
     for i in (7, 1031, 4095):
         assert np.array_equal(ids[i], ids[i - 1]) and np.array_equal(pred[i], pred[i - 1])
+    s.close()
 
 
 @pytest.mark.parametrize("kern", ["tc", "pair"])
@@ -366,5 +404,5 @@ def test_seeded_large_k(kern, k):
     if not kernel_available(s, kern):
         pytest.skip(f"{kern} kernel unavailable")
     ids, sc, pred = run(s, q, k)
-    assert_parity(compare(q, x, a, k, ids, sc, pred))
+    assert_parity(compare(q, x, a, k, ids, sc, pred), f"c2[200k] seeded k={k} {kern}")
     assert ids[3, 0] == 16 * 7 and ids[4, 0] == 16 * 7 + 1

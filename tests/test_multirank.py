@@ -4,8 +4,12 @@ They check the exchange protocol the library implements over NCCL (DESIGN.md §8
 with the oracle standing in for each rank's kernels:
   * the NCCL unique id bootstrap delivers identical bytes to every rank;
   * S5: merging the per-rank top-k lists (all-gather) gives exactly the unsharded top-k;
-  * S7: the all-reduce of owned winner rows (zeros elsewhere) reproduces every winner
-    row bit-exactly on every rank, so the prediction equals the one-GPU prediction.
+  * S7: every rank reduces only the winners it OWNS into a partial prediction P_g; the
+    partials are exchanged (all-gather, or all-to-all by query slice + broadcast of the
+    finished slices -- the two layouts runtime.cu picks by size) and summed in rank order,
+    so every rank holds the same prediction, equal to the unsharded one.
+The library's own implementation of this protocol (runtime.cu stage functions) runs on
+one GPU through a loopback group: tests/test_gpu_loopback.py.
 """
 import os
 import socket
@@ -87,17 +91,37 @@ def _exchange(rank, world):
         order = sorted(range(merged.shape[1]), key=lambda r: (-merged[i, r, 0], merged[i, r, 1]))[:k]
         top_ids[i] = merged[i, order, 1].astype(np.int64)
         top_sc[i] = merged[i, order, 0]
-    # S7: owned winner rows, zeros elsewhere, summed across ranks
+    # S6 + partial S7: weights from the (identical) merged scores; P_g over owned winners
     L, E = c.layers, c.experts
-    rows = np.zeros((B, k, L, E), np.float32)
+    part = np.zeros((B, L, E))
     for i in range(B):
+        w = oracle.softmax(top_sc[i])
         for r in range(k):
             j = top_ids[i, r] - off
             if 0 <= j < n:
-                rows[i, r] = a[j]
-    t = torch.from_numpy(rows)
-    dist.all_reduce(t)
-    return top_ids, top_sc, t.numpy()
+                part[i] += w[r] * a[j].astype(np.float64)
+    # exchange 2, layout 1: all-gather of whole partials, rank-order sum
+    allp = [torch.zeros(B, L, E, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(allp, torch.from_numpy(part))
+    pred_ag = sum(p.numpy() for p in allp)  # g ascending
+    # layout 2: rank g owns query slice [B g / G, B (g+1) / G): it receives every rank's
+    # partial of its slice (all_gather stands in for the all-to-all), sums in rank order,
+    # then the finished slices are broadcast from their owners
+    lo = [B * g // world for g in range(world + 1)]
+    mine = [torch.zeros(lo[rank + 1] - lo[rank], L, E, dtype=torch.float64) for _ in range(world)]
+    for g in range(world):
+        src = torch.from_numpy(part[lo[g]:lo[g + 1]].copy())
+        got = [torch.zeros_like(src) for _ in range(world)]
+        dist.all_gather(got, src)
+        if g == rank:
+            mine = got
+    pred_a2a = np.zeros((B, L, E))
+    pred_a2a[lo[rank]:lo[rank + 1]] = sum(t.numpy() for t in mine)
+    for g in range(world):
+        sl = torch.from_numpy(pred_a2a[lo[g]:lo[g + 1]].copy())
+        dist.broadcast(sl, g)
+        pred_a2a[lo[g]:lo[g + 1]] = sl.numpy()
+    return top_ids, top_sc, pred_ag, pred_a2a
 
 
 def test_sharded_exchange_equals_unsharded_oracle():
@@ -114,14 +138,11 @@ def test_sharded_exchange_equals_unsharded_oracle():
     q = gen.queries(c.store_seed, c.query_seed, n_total, c.dim, B, mode=1)
     ids, sc, pred = oracle.sps(q, x, a, k)
     for r in (0, 1):
-        top_ids, top_sc, rows = out[r]
+        top_ids, top_sc, pred_ag, pred_a2a = out[r]
         np.testing.assert_array_equal(top_ids, ids)          # exact global top-k
         np.testing.assert_array_equal(top_sc, sc)
-        np.testing.assert_array_equal(rows, a[ids])          # exact winner rows on every rank
-        # the prediction from the gathered rows equals the one-GPU prediction
-        w = np.stack([oracle.softmax(top_sc[i]) for i in range(B)])
-        p = np.einsum("br,brle->ble", w, rows.astype(np.float64))
-        np.testing.assert_allclose(p, pred, rtol=0, atol=1e-15)
+        np.testing.assert_allclose(pred_ag, pred, rtol=0, atol=1e-14)   # owner partials, summed
+        np.testing.assert_array_equal(pred_a2a, pred_ag)     # both layouts: the same rank-order sum
     for u, v in zip(out[0], out[1]):
         np.testing.assert_array_equal(u, v)                   # identical on every rank
 
@@ -131,7 +152,14 @@ def test_shard_range_matches_generator():
     sys.path.insert(0, ROOT)
     import gen
     from paper_2512_18674_b200.dist import shard_range
-    for n in (1, 5, 1000, 10_000_000):
-        for w in (1, 2, 4, 8):
+    for n in (1, 5, 9, 1000, 10_000_000):
+        for w in (1, 2, 3, 4, 8):
+            parts = [shard_range(n, w, r) for r in range(w)]
             for r in range(w):
-                assert shard_range(n, w, r) == gen.shard_range(n, w, r)
+                assert parts[r] == gen.shard_range(n, w, r)
+            assert parts[0][0] == 0 and sum(p[1] for p in parts) == n   # tiles [0, n)
+            for r in range(1, w):
+                assert parts[r][0] == parts[r - 1][0] + parts[r - 1][1]
+            if n >= w:
+                assert min(p[1] for p in parts) >= 1                    # balanced: none empty
+                assert max(p[1] for p in parts) - min(p[1] for p in parts) <= 1

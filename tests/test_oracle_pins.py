@@ -246,6 +246,39 @@ def test_whole_path_vs_numpy_scipy_bruteforce():
         np.testing.assert_array_equal(pred[i], pred[i - 1])
 
 
+@pytest.mark.parametrize("n,nthreads", [(5003, 1), (5003, 7), (12289, 8), (12289, 64), (20000, 256)])
+def test_threaded_row_split_vs_numpy(n, nthreads):
+    """The oracle's pthread row split (all_scores, N >= 1024) against numpy brute force:
+    every score of the [B, N] matrix, and the whole path (select, softmax, predict) with
+    exact duplicate rows planted across the per-thread range boundaries, so an off-by-one
+    in a thread's [lo, hi) (a dropped, doubled or shifted row) or a tie broken by thread
+    order instead of the lower id fails here."""
+    c = gen.CONFIGS["c2"]
+    xb = gen.store_emb(c.store_seed, n, c.dim).copy()
+    act = gen.store_act(c.store_seed, n, c.layers, c.experts, c.moe_topk)
+    qb = gen.queries(c.store_seed, c.query_seed, n, c.dim, 6, mode=1)
+    per = -(-n // nthreads)
+    for b in range(per, n, per):  # rows on both sides of each thread boundary
+        xb[b] = xb[b - 1]
+    qb[0] = xb[per - 1]            # a query whose best matches straddle a boundary
+    x = gen.bf16_bits_to_f32(xb).astype(np.float64)
+    q = gen.bf16_bits_to_f32(qb).astype(np.float64)
+    ref = (q @ x.T) / (np.linalg.norm(q, axis=1)[:, None] * np.linalg.norm(x, axis=1)[None] + SIGMA)
+    s = oracle.scores(qb, xb, nthreads=nthreads)
+    np.testing.assert_allclose(s, ref, rtol=0, atol=1e-12)
+    k = 12
+    ids, sc, pred = oracle.sps(qb, xb, act, k, nthreads=nthreads)
+    for i in range(qb.shape[0]):
+        order = np.lexsort((np.arange(n), -s[i]))[:k]   # library sort of the (independent) scores
+        order_ref = np.lexsort((np.arange(n), -ref[i]))[:k]
+        assert list(ids[i]) == list(order) == list(order_ref)
+        w = scipy_softmax(ref[i, order])
+        np.testing.assert_allclose(pred[i], np.einsum("r,rle->le", w, act[order].astype(np.float64)),
+                                   rtol=0, atol=1e-12)
+    if per < n:
+        assert ids[0, 0] == per - 1 and ids[0, 1] == per  # duplicate pair: lower id first
+
+
 # ---------------------------------------------------------------- NEXT-N4 JS divergence
 
 def test_js_divergence_pins():
