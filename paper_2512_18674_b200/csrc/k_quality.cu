@@ -39,7 +39,8 @@ __global__ void __launch_bounds__(256) k_js(const float* __restrict__ P, const f
 cudaError_t launch_js(const float* P, const float* Q, int64_t q_stride, int B, int L, int E, float* out,
                       cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
-  cudaError_t e = set_smem_attrs_once((const void*)k_js, 0);
+  // remoe_js_divergence admits L * 4 <= 200 KB of per-layer values: opt in to that much
+  cudaError_t e = set_smem_attrs_once((const void*)k_js, 200 * 1024);
   if (e != cudaSuccess) return e;
   k_js<<<B, 256, (size_t)L * sizeof(float), st>>>(P, Q, q_stride, L, E, out);
   return cudaGetLastError();

@@ -25,9 +25,9 @@
 #include <stdlib.h>
 
 #include <type_traits>
+#include <vector>
 
 #include "common.cuh"
-#include <vector>
 
 #include "host_util.h"
 #include "kernels.h"
@@ -73,6 +73,24 @@ struct TcArgs {
                            // slab of nq queries stores only ceil(nq/8) 8-row atoms
   unsigned long long* trace;  // REMOE_TC_TRACE: [grid][16] globaltimer stamps
   unsigned long long* stats;  // REMOE_TC_STATS: [0] candidate columns, [1] inserts, [2] chunks with a candidate
+  // ---- in-kernel threshold seeding (DESIGN.md §7 "threshold seeding"): each CTA first
+  // scans its share of the sample tiles (a tiled copy of every s-th store row, TcSeed)
+  // with a small register tracker per state, publishes the state's h-th best sample key,
+  // and the last CTA of the slab to arrive sets every query's shared threshold to
+  // (the r-th largest published key) - 1, r * h >= k: at least k real keys of the store
+  // are >= that key, so it is a lower bound of the final k-th best (strict after -1).
+  const uint16_t* seed_xt;   // tiled sample (nullptr: no seeding)
+  const float* seed_xn;      // sample norms [n tiles * 128]
+  int seed_n_stiles;         // sample tiles scanned (a prefix of the segments)
+  int seed_nseg;
+  int seed_t0[5];            // first sample tile of segment g (seed_t0[nseg] = total)
+  int64_t seed_count[4];     // rows of segment g: store rows off + i * stride, i < count
+  int64_t seed_off[4];
+  int64_t seed_stride[4];
+  int seed_h, seed_r;
+  uint64_t* seed_keys;       // [nq][2 * gridDim.x] published h-th keys (this launch's queries)
+  unsigned* seed_sync;       // [2 * gridDim.y]: per slab arrival count, generation
+  long long seed_wait_ns;    // how long a CTA waits for the seeded thresholds (0: no wait)
 };
 }  // namespace
 
@@ -80,6 +98,18 @@ struct TcArgs {
 // lanes 0-15 of each 32-lane TMEM quarter (row r -> lane 32*(r/16) + r%16).  Slab row
 // r = R*q + l (R = M/4 rows per quarter) holds query m = 4*l + q, so a batch smaller than
 // M spreads over all four epilogue quarters instead of filling the first one.
+// The h-th best key of a register tracker (h <= K), by selects (no run-time register index).
+// The list is sorted descending, so the h-th best is the minimum of the first h entries: a
+// min-reduction (a select chain on j == h - 1 gets turned into a dynamic register index,
+// which demotes the whole tracker to the local stack).
+template <int K>
+__device__ __forceinline__ uint64_t tracker_key(const RegTopk<K>& tr, int h) {
+  uint64_t kh = tr.L[0];
+#pragma unroll
+  for (int j = 1; j < K; ++j) kh = umin64(kh, j < h ? tr.L[j] : ~0ull);
+  return kh;
+}
+
 #define TRACE(idx)                                                                              \
   do {                                                                                          \
     if (p.trace && (threadIdx.x & 31) == 0) {                                                   \
@@ -107,16 +137,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = bars + 2 * NST + kAcc;
   uint64_t* cempty = bars + 2 * NST + 2 * kAcc;  // [NST] cluster-wide "slot free" (leader CTA)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NST + 2 * kAcc);
-  // [8 warps][128] x-norms, 16-byte aligned for ld/st.shared.v4
+  volatile int& s_seed_last = *reinterpret_cast<int*>(bars + 3 * NST + 2 * kAcc + 1);  // free slot before sXn
   // [2 parities][2 buffers][128] tile x-norms, shared by the 4 warps of a parity
   float* sXn = reinterpret_cast<float*>(bars + ((3 * NST + 2 * kAcc + 2 + 1) & ~1));
-  // [128] per-query threshold shared by the two parity states of the CTA (register top-k)
+  // [M] per-query threshold shared by the two parity states of the CTA (register top-k)
   unsigned long long* pair_thr = reinterpret_cast<unsigned long long*>(sXn + 4 * kTileN);  // [M]
   uint64_t* sBuf = reinterpret_cast<uint64_t*>(pair_thr + M);  // [256][CAP] if p.smem_bufs
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t n_tiles = (p.n_rows + kTileN - 1) / kTileN;
+  // This CTA's tile sequence: its sample tiles (threshold seeding) first, then its store
+  // tiles; the TMA producer, the MMA issuer and the epilogue walk the same sequence.
+  const bool seeding = p.seed_xt != nullptr;
+  const int64_t ns_cta = (seeding && p.seed_n_stiles > (int)blockIdx.x)
+                             ? (p.seed_n_stiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int64_t n_it = ns_cta + (n_tiles - 1 - (int64_t)blockIdx.x) / gridDim.x + 1;  // grid.x <= n_tiles
+  auto tile_of = [&](int64_t i) -> int64_t {
+    return (int64_t)blockIdx.x + (i < ns_cta ? i : i - ns_cta) * (int64_t)gridDim.x;
+  };
   TRACE(0);
   pdl_trigger();  // the merge kernel may be scheduled as SMs free up
   // Query slab of this CTA (blockIdx.y).  With several slabs, the CTAs of every slab walk
@@ -192,16 +231,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
       int it = 0;
-      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int64_t i = 0; i < n_it; ++i) {
+        const bool smp = i < ns_cta;
+        const int64_t t = tile_of(i);
         for (int j = 0; j < nkb; ++j, ++it) {
           const int kb = kb_at(j, nkb, p.kb_order);
           const int s = it % NST;
           const uint32_t ph = (uint32_t)(it / NST) & 1u;
           mbar_wait(&empty[s], ph ^ 1u);  // this CTA's MMA is done with the slot
           mbar_arrive_expect_tx(&full[s], kStageBytes);
-          // tiled store: box (t, kb) is 16 KB contiguous in HBM, already in the swizzled
-          // UMMA layout, so a 1-D bulk copy streams it (no 128 B-per-row DRAM pattern)
-          const uint16_t* src = p.xt ? p.xt + ((size_t)t * nkb + kb) * (kStageBytes / 2) : nullptr;
+          // tiled store / sample: box (t, kb) is 16 KB contiguous in HBM, already in the
+          // swizzled UMMA layout, so a 1-D bulk copy streams it (no 128 B-per-row pattern)
+          const uint16_t* src = smp ? p.seed_xt + ((size_t)t * nkb + kb) * (kStageBytes / 2)
+                                    : p.xt ? p.xt + ((size_t)t * nkb + kb) * (kStageBytes / 2) : nullptr;
           if (C == 1) {
             if (src) bulk_g2s(sB + (size_t)s * kStageBytes, src, kStageBytes, &full[s]);
             else tma_load_2d(sB + (size_t)s * kStageBytes, &tmap_x, kb * kBlockK, (int)(t * kTileN), &full[s]);
@@ -226,9 +268,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((nn >> 3) << 17) |
                              ((uint32_t)(M >> 4) << 24);
       const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
-      int it = 0, i = 0;
-      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-        const int acc = i % kAcc;
+      int it = 0;
+      for (int64_t i = 0; i < n_it; ++i) {
+        const int acc = (int)(i % kAcc);
         const uint32_t aph = (uint32_t)(i / kAcc) & 1u;
         mbar_wait(&tempty[acc], aph ^ 1u);
         tc_fence_after();
@@ -266,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // i.e. two top-k states per query per CTA.  For M = 64 the queries sit in lanes
     // 0-15 of a quarter and lanes 16-31 idle.
     //
-    // Per 32-column chunk the common path is branch-free: x-norms come from a per-warp
+    // Per 32-column chunk the common path is branch-free: x-norms come from a per-parity
     // shared-memory copy (ld.shared.v4 broadcasts), and a conservative fp32 test
     // dot >= tlim * (|q||x| + sigma) builds a 32-bit candidate mask; only columns in
     // the mask (rare once the threshold has settled) get the IEEE division, the key
@@ -293,34 +335,135 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (KR > 0) tk.init(p.k, active ? gthr_sl + m : nullptr);
     else tk.init(buf, active ? gthr_sl + m : nullptr);
     if (!active) tk.tlim = __int_as_float(0x7f800000);  // +inf: never a candidate
-    // the tile's |x_j| (lane l loads rows 4l..4l+3) are loaded one tile ahead
-    auto load_xn = [&](int64_t t) {
-      float4 x = make_float4(1.f, 1.f, 1.f, 1.f);
-      if (t >= n_tiles) return x;
-      const int64_t r0 = t * kTileN;
-      const int nv = (int)((p.n_rows - r0) < kTileN ? (p.n_rows - r0) : kTileN);
-      if (4 * lane + 3 < nv) {
-        x = __ldg(reinterpret_cast<const float4*>(p.xnorm + r0) + lane);
+    // seeding tracker: the best kHS keys of this state's sample tiles (h <= kHS of them count)
+    constexpr int kHS = KR > 0 ? 4 : 8;
+    RegTopk<kHS> tr;
+    tr.init(kHS, nullptr);
+    if (!active) tr.tlim = __int_as_float(0x7f800000);
+
+    // tile i of the sequence: x-norm source, valid rows, global id of column j = gbase + j * gstride
+    struct TileInfo { const float* xn; int nvalid; int64_t gbase, gstride; };
+    auto tile_info = [&](int64_t i) -> TileInfo {
+      TileInfo ti;
+      const int64_t t = tile_of(i);
+      if (i < ns_cta) {
+        // the tile's segment, by selects over the (parameter-space) segment arrays: a
+        // run-time index would copy them to the local stack
+        int64_t t0 = 0, cnt = 0, off = 0, str = 1;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          if (g < p.seed_nseg && t >= p.seed_t0[g]) {
+            t0 = p.seed_t0[g]; cnt = p.seed_count[g]; off = p.seed_off[g]; str = p.seed_stride[g];
+          }
+        }
+        const int64_t li = (t - t0) * kTileN;
+        ti.xn = p.seed_xn + t * kTileN;
+        ti.nvalid = (int)min((int64_t)kTileN, cnt - li);
+        ti.gstride = str;
+        ti.gbase = p.gid_offset + off + li * str;
       } else {
-        if (4 * lane + 0 < nv) x.x = __ldg(p.xnorm + r0 + 4 * lane + 0);
-        if (4 * lane + 1 < nv) x.y = __ldg(p.xnorm + r0 + 4 * lane + 1);
-        if (4 * lane + 2 < nv) x.z = __ldg(p.xnorm + r0 + 4 * lane + 2);
+        const int64_t row0 = t * kTileN;
+        ti.xn = p.xnorm + row0;
+        ti.nvalid = (int)min((int64_t)kTileN, p.n_rows - row0);
+        ti.gstride = p.gid_stride;
+        ti.gbase = p.gid_offset + row0 * p.gid_stride;
+      }
+      return ti;
+    };
+    // the tile's |x_j| (lane l loads rows 4l..4l+3), loaded one tile ahead
+    auto load_xn = [&](int64_t i) {
+      float4 x = make_float4(1.f, 1.f, 1.f, 1.f);
+      if (i >= n_it) return x;
+      const TileInfo ti = tile_info(i);
+      if (4 * lane + 3 < ti.nvalid) {
+        x = __ldg(reinterpret_cast<const float4*>(ti.xn) + lane);
+      } else {
+        if (4 * lane + 0 < ti.nvalid) x.x = __ldg(ti.xn + 4 * lane + 0);
+        if (4 * lane + 1 < ti.nvalid) x.y = __ldg(ti.xn + 4 * lane + 1);
+        if (4 * lane + 2 < ti.nvalid) x.z = __ldg(ti.xn + 4 * lane + 2);
       }
       return x;
     };
-    const int64_t tstep = 2 * (int64_t)gridDim.x;
-    float4 xv_next = load_xn(blockIdx.x + parity * (int64_t)gridDim.x);
+    // Seeding hand-off, once per thread, before its first store tile: publish the state's
+    // h-th best sample key; the last CTA of the slab to arrive computes every query's
+    // seeded threshold, the others wait for it (bounded: a CTA that times out goes on
+    // with its own thresholds, which is always exact, and picks the seeded ones up later).
+    auto seed_sync = [&](uint64_t kh) {
+      const int G2 = 2 * (int)gridDim.x;
+      if (active) p.seed_keys[(size_t)(slab * M + m) * G2 + 2 * blockIdx.x + parity] = kh;
+      __threadfence();
+      asm volatile("bar.sync 10, %0;" ::"n"(kEpiWarps * 32) : "memory");
+      unsigned* cnt = p.seed_sync + 2 * slab;
+      unsigned gen0 = 0;
+      if (e == 0 && lane == 0) {
+        gen0 = *reinterpret_cast<volatile unsigned*>(cnt + 1);
+        __threadfence();
+        s_seed_last = atomicAdd(cnt, 1u) == gridDim.x - 1u;
+      }
+      asm volatile("bar.sync 10, %0;" ::"n"(kEpiWarps * 32) : "memory");
+      if (s_seed_last) {
+        __threadfence();
+        // r-th largest of the 2 * grid.x published keys of each query: warp e takes queries
+        // e, e + 8, ...; iterative extraction of the maximum (keys are distinct or 0)
+        for (int mm = e; mm < nq; mm += kEpiWarps) {
+          const uint64_t* kp = p.seed_keys + (size_t)(slab * M + mm) * G2;
+          uint64_t v[10];
+#pragma unroll
+          for (int u = 0; u < 10; ++u) v[u] = lane + 32 * u < G2 ? __ldcg(kp + lane + 32 * u) : 0ull;
+          uint64_t T = 0;
+          for (int r = 0; r < p.seed_r; ++r) {
+            uint64_t mx = v[0];
+#pragma unroll
+            for (int u = 1; u < 10; ++u) mx = umax64(mx, v[u]);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) mx = umax64(mx, __shfl_xor_sync(kFull, mx, off));
+            T = mx;
+            if (T == 0) break;
+#pragma unroll
+            for (int u = 0; u < 10; ++u) v[u] = v[u] == T ? 0ull : v[u];
+          }
+          if (T != 0 && lane == 0) atomicMax(gthr_sl + mm, (unsigned long long)(T - 1));
+        }
+        __threadfence();
+        asm volatile("bar.sync 10, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        if (e == 0 && lane == 0) {
+          *reinterpret_cast<volatile unsigned*>(cnt) = 0u;
+          __threadfence();
+          atomicAdd(cnt + 1, 1u);
+        }
+      } else if (p.seed_wait_ns > 0) {
+        if (e == 0 && lane == 0) {
+          unsigned long long t0, t1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          while (*reinterpret_cast<volatile unsigned*>(cnt + 1) == gen0) {
+            __nanosleep(256);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if ((long long)(t1 - t0) > p.seed_wait_ns) break;
+          }
+          __threadfence();
+        }
+        asm volatile("bar.sync 10, %0;" ::"n"(kEpiWarps * 32) : "memory");
+      }
+    };
+    bool synced = !seeding;
+    float4 xv_next = load_xn(parity);
     uint64_t pair_pub = 0;  // last value this state shared with its parity partner
     uint64_t gt_next = tk.peek_shared();  // shared threshold, also read one tile ahead
-    int i = parity;
-    for (int64_t t = blockIdx.x + parity * (int64_t)gridDim.x; t < n_tiles; t += tstep, i += 2) {
-      const int acc = i % kAcc;
+    for (int64_t i = parity; i < n_it; i += 2) {
+      const bool smp = i < ns_cta;
+      if (!smp && !synced) {
+        TRACE(3);
+        seed_sync(tracker_key(tr, p.seed_h));
+        TRACE(10);
+        synced = true;
+        gt_next = tk.peek_shared();
+      }
+      const int acc = (int)(i % kAcc);
       const uint32_t aph = (uint32_t)(i / kAcc) & 1u;
-      const int64_t row0 = t * kTileN;
-      const int nvalid = (int)((p.n_rows - row0) < kTileN ? (p.n_rows - row0) : kTileN);
+      const TileInfo ti = tile_info(i);
       const float4 xv = xv_next;
       const uint64_t gt = gt_next;
-      xv_next = load_xn(t + tstep);
+      xv_next = load_xn(i + 2);
       gt_next = tk.peek_shared();
       if (p.epi_sleep) mbar_wait_sleep(&tfull[acc], aph);
       else mbar_wait(&tfull[acc], aph);
@@ -328,12 +471,48 @@ __global__ void __launch_bounds__(kThreads, 1)
       reinterpret_cast<float4*>(xs)[lane] = xv;  // the 4 warps write identical values
       asm volatile("bar.sync %0, 128;" ::"r"(7 + parity) : "memory");  // the parity's 4 warps
       if (i < 2) TRACE(7);
-      if (active) tk.raise(gt);
+      if (active && !smp) tk.raise(gt);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kTileN);
       if (p.dbg & 2) {  // debug (REMOE_TC_DBG=2): release the accumulator unread (wrong results)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
+        continue;
+      }
+      if (smp) {
+        // ---- a sample tile: only the tracker (the store pass scans these rows again)
+#pragma unroll 1
+        for (int c = 0; c < kTileN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tbase + c * 32, v);
+          tmem_wait_ld();
+          if (c == kTileN / 32 - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
+          const float* xc = xs + c * 32;
+          unsigned mask = 0;
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4) {
+            const float4 x4 = lds128f(xc + 4 * j4);
+            const float xx[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int j = 4 * j4 + u;
+              mask |= (tr.may_pass(__uint_as_float(v[j]), __fmaf_rn(qn, xx[u], p.sigma)) ? 1u : 0u) << j;
+            }
+          }
+          const int left = ti.nvalid - c * 32;
+          if (left < 32) mask &= left > 0 ? ((1u << left) - 1u) : 0u;
+          while (mask) {
+            const int j = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const float den = __fmaf_rn(qn, xc[j], p.sigma);
+            const float vj = __uint_as_float(sel32(v, j));
+            if (vj >= tr.tlim * den) tr.insert(make_key(__fdiv_rn(vj, den), ti.gbase + (c * 32 + j) * ti.gstride));
+          }
+        }
         continue;
       }
 #pragma unroll 1
@@ -364,11 +543,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             mask |= (tk.may_pass(__uint_as_float(v[j]), den) ? 1u : 0u) << j;
           }
         }
-        const int left = nvalid - c * 32;
+        const int left = ti.nvalid - c * 32;
         if (left < 32) mask &= left > 0 ? ((1u << left) - 1u) : 0u;
         if constexpr (KR > 0) {
           if (__any_sync(kFull, mask != 0)) {
-            const int64_t gbase = p.gid_offset + (row0 + c * 32) * p.gid_stride;
+            const int64_t gbase = ti.gbase + (int64_t)(c * 32) * ti.gstride;
             if (p.stats) {
               atomicAdd(p.stats + 0, (unsigned long long)__popc(mask));
               if (lane == 0) atomicAdd(p.stats + 2, 1ull);
@@ -379,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float den = __fmaf_rn(qn, xc[j], p.sigma);
               const float vj = __uint_as_float(sel32(v, j));
               if (vj >= tk.tlim * den) {
-                const int64_t gid = gbase + j * p.gid_stride;
+                const int64_t gid = gbase + j * ti.gstride;
                 const uint64_t key = make_key(__fdiv_rn(vj, den), gid);
                 if (p.stats && key > tk.thr) atomicAdd(p.stats + 1, 1ull);
                 tk.insert(key);
@@ -396,7 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // many candidates (the first tiles, before the thresholds settle): compute all
             // keys of the chunk at once and append them (room for 32 guaranteed first)
             tk.ensure_room(32, p.k);
-            const int64_t gbase = p.gid_offset + (row0 + c * 32) * p.gid_stride;
+            const int64_t gbase = ti.gbase + (int64_t)(c * 32) * ti.gstride;
 #pragma unroll
             for (int j4 = 0; j4 < 8; ++j4) {
               const float4 x4 = lds128f(xc + 4 * j4);
@@ -406,20 +585,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int j = 4 * j4 + u;
                 if ((mask >> j) & 1u) {
                   const float den = __fmaf_rn(qn, xx[u], p.sigma);
-                  const int64_t gid = gbase + j * p.gid_stride;
+                  const int64_t gid = gbase + j * ti.gstride;
                   tk.append(make_key(__fdiv_rn(__uint_as_float(v[j]), den), gid));
                 }
               }
             }
           } else if (__any_sync(kFull, mask != 0)) {
-            const int64_t gbase = p.gid_offset + (row0 + c * 32) * p.gid_stride;
+            const int64_t gbase = ti.gbase + (int64_t)(c * 32) * ti.gstride;
             while (__any_sync(kFull, mask != 0)) {
               uint64_t key = 0;
               if (mask) {
                 const int j = __ffs(mask) - 1;
                 mask &= mask - 1;
                 const float den = __fmaf_rn(qn, xc[j], p.sigma);
-                const int64_t gid = gbase + j * p.gid_stride;
+                const int64_t gid = gbase + j * ti.gstride;
                 key = make_key(__fdiv_rn(__uint_as_float(sel32(v, j)), den), gid);
               }
               tk.push(key, p.k);
@@ -429,6 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if constexpr (KR > 0) tk.publish();
     }
+    if (!synced) seed_sync(tracker_key(tr, p.seed_h));  // this parity had no store tile: still takes part once
     TRACE(8);
     if (KR > 0 && p.merge_in_cta) {
       // Merge the two parity states of each query inside the CTA (one list per CTA per
@@ -490,6 +670,58 @@ cudaError_t tc_tile_store(const uint16_t* x, int64_t n_rows, int dim, uint16_t* 
   if (dim % kBlockK != 0 || n_rows <= 0) return cudaErrorInvalidValue;
   k_tile_store<<<1184, 256, 0, st>>>(reinterpret_cast<const uint4*>(x), n_rows, dim, reinterpret_cast<uint4*>(xt));
   return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ seeding sample
+// out row i = x[src[i]] (src[i] < 0: a zero row), its norm xn[src[i]] (1 for padding).
+__global__ void k_gather_sample(const uint4* __restrict__ x, const float* __restrict__ xnorm,
+                                const int64_t* __restrict__ src, int64_t n, int dim, uint4* __restrict__ out,
+                                float* __restrict__ out_norm) {
+  const int cpr = dim / 8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n * cpr; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / cpr;
+    const int c = (int)(i - row * cpr);
+    const int64_t r = src[row];
+    out[i] = r >= 0 ? x[r * cpr + c] : make_uint4(0u, 0u, 0u, 0u);
+    if (c == 0) out_norm[row] = r >= 0 ? xnorm[r] : 1.f;
+  }
+}
+
+remoe_status_t tc_seed_build(TcSeed* sd, const uint16_t* x, const float* xnorm, int64_t n_rows, int dim,
+                             cudaStream_t st, void* (*alloc)(void*, size_t), void* actx) {
+  // segments: rows 64j, 64j+32, 32j+16, 16j+8 (a prefix of g + 1 segments = every
+  // (64 >> g)-th row), each padded to whole 128-row tiles
+  static const int64_t off[4] = {0, 32, 16, 8}, stride[4] = {64, 64, 32, 16};
+  sd->n_seg = 0;
+  int64_t tiles = 0;
+  std::vector<int64_t> src;
+  for (int g = 0; g < 4; ++g) {
+    const int64_t cnt = n_rows > off[g] ? (n_rows - off[g] + stride[g] - 1) / stride[g] : 0;
+    if (cnt == 0) break;
+    sd->seg_t0[g] = (int)tiles;
+    sd->seg_count[g] = cnt;
+    sd->seg_off[g] = off[g];
+    sd->seg_stride[g] = stride[g];
+    const int64_t nt = (cnt + kTileN - 1) / kTileN;
+    for (int64_t i = 0; i < nt * kTileN; ++i) src.push_back(i < cnt ? off[g] + i * stride[g] : -1);
+    tiles += nt;
+    sd->n_seg = g + 1;
+  }
+  sd->seg_t0[sd->n_seg] = (int)tiles;
+  if (sd->n_seg == 0) return REMOE_OK;
+  const int64_t rows = tiles * kTileN;
+  int64_t* d_src = static_cast<int64_t*>(alloc(actx, rows * 8));
+  uint16_t* tmp = static_cast<uint16_t*>(alloc(actx, (size_t)rows * dim * 2));
+  sd->xt = static_cast<uint16_t*>(alloc(actx, (size_t)rows * dim * 2));
+  sd->xn = static_cast<float*>(alloc(actx, (size_t)rows * 4));
+  if (!d_src || !tmp || !sd->xt || !sd->xn) return REMOE_ERR_OOM;
+  if (cudaMemcpyAsync(d_src, src.data(), rows * 8, cudaMemcpyHostToDevice, st) != cudaSuccess) return REMOE_ERR_CUDA;
+  k_gather_sample<<<1184, 256, 0, st>>>(reinterpret_cast<const uint4*>(x), xnorm, d_src, rows, dim,
+                                        reinterpret_cast<uint4*>(tmp), sd->xn);
+  if (cudaGetLastError() != cudaSuccess) return REMOE_ERR_CUDA;
+  if (tc_tile_store(tmp, rows, dim, sd->xt, st) != cudaSuccess) return REMOE_ERR_CUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return REMOE_ERR_CUDA;
+  return REMOE_OK;
 }
 
 // ------------------------------------------------------------------ host side
@@ -636,7 +868,7 @@ static cudaError_t launch_tc_m(const TcPlan* t, const TcArgs& a, dim3 g, cudaStr
 remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc, int k, float sigma,
                        const float* xnorm, int64_t n_rows, int64_t gid_offset, int64_t gid_stride,
                        uint64_t* cand_buf, unsigned long long* gthr, uint64_t* lists, cudaStream_t st,
-                       int* launches, int* lists_per_query) {
+                       int* launches, int* lists_per_query, const TcSeedUse* seed) {
   if (!t->ok) return REMOE_ERR_UNSUPPORTED;
   // M = 128 when the 128-query slab still leaves >= 4 stages, else 64.  Candidate
   // buffers go to shared memory when that still leaves >= 4 stages.
@@ -685,6 +917,24 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
     a.kb_order = kn.kb_order;
     a.slab_rows = SR;
     a.dbg = kn.dbg;
+    if (seed && t->xt && 2 * ctas_per_slab <= 320) {
+      const TcSeed& sd = *seed->store;
+      a.seed_xt = sd.xt;
+      a.seed_xn = sd.xn;
+      a.seed_n_stiles = seed->n_stiles;
+      a.seed_nseg = sd.n_seg;
+      for (int g = 0; g <= sd.n_seg; ++g) a.seed_t0[g] = sd.seg_t0[g];
+      for (int g = 0; g < sd.n_seg; ++g) {
+        a.seed_count[g] = sd.seg_count[g];
+        a.seed_off[g] = sd.seg_off[g];
+        a.seed_stride[g] = sd.seg_stride[g];
+      }
+      a.seed_h = seed->h;
+      a.seed_r = seed->r;
+      a.seed_keys = sd.keys + (size_t)s0 * 2 * ctas_per_slab;
+      a.seed_sync = sd.sync + 2 * sl0;
+      a.seed_wait_ns = sd.wait_ns;
+    }
     if (kn.stats) {  // debug counters (this plan's buffer)
       if (!t->stats_buf && cudaMalloc(&t->stats_buf, 3 * 8) != cudaSuccess) return REMOE_ERR_OOM;
       cudaMemsetAsync(t->stats_buf, 0, 3 * 8, st);
@@ -707,10 +957,9 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
       for (int c = 0; c < n_cta; ++c) if (h[c * 16] && h[c * 16] < t0) t0 = h[c * 16];
       fprintf(stderr, "[remoe] tc trace (us from first CTA start; CTA 0 | max over CTAs): nq %d k %d tiles %lld\n",
               a.nq, k, (long long)((n_rows + kTileN - 1) / kTileN));
-      const char* names[10] = {"start", "setup", "slab", "-", "mma first full", "mma tile0 commit", "epi pdl_wait",
-                               "epi first tfull", "epi loop done", "end"};
-      for (int i = 0; i < 10; ++i) {
-        if (i == 3) continue;
+      const char* names[11] = {"start", "setup", "slab", "seed sync in", "mma first full", "mma tile0 commit",
+                               "epi pdl_wait", "epi first tfull", "epi loop done", "end", "seed sync out"};
+      for (int i = 0; i < 11; ++i) {
         unsigned long long mx = 0;
         for (int c = 0; c < n_cta; ++c) if (h[c * 16 + i] > mx) mx = h[c * 16 + i];
         fprintf(stderr, "  %-18s %9.2f | %9.2f\n", names[i], h[i] ? (h[i] - t0) / 1e3 : -1.0,

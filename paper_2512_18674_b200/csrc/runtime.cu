@@ -150,8 +150,11 @@ struct remoe_sps {
     remoe::TcPlan tc{};            // strided tensor map over the store
     float* xns = nullptr;          // their norms
   };
-  SeedSample seeds[4];  // strides 64, 32, 16, 8 (larger k takes a denser sample)
+  SeedSample seeds[4];  // strides 64, 32, 16, 8 (larger k takes a denser sample): CTA-pair scan
   int n_seeds = 0;
+  // the tensor-core scan seeds inside the kernel from a tiled sample (TcSeed, k_scan_tc)
+  remoe::TcSeed seed_store{};
+  bool seed_inkernel = true;  // REMOE_SEED_INKERNEL=0: the separate seed-scan launch instead (A/B)
   uint64_t* seed_top = nullptr;
   // -1 auto: seed when k > 32 or B >= seed_min_b; 1 always (REMOE_SEED=1); 0 never
   // (REMOE_SEED=0).  Without a seed every top-k state (a CTA's rows for one query) starts
@@ -457,11 +460,29 @@ static remoe_status_t build_local(remoe_sps* h, const uint16_t* emb, const float
       if (sd.tc.ok) ++h->n_seeds;
     }
   }
+  // in-kernel seeding sample of the tensor-core scan: every 64th/32nd/16th/8th row, tiled
+  if (h->tc.ok && h->xt && c.n_local >= 32768) {
+    auto al = [](void* ctx, size_t bytes) -> void* {
+      void* p = nullptr;
+      return static_cast<remoe_sps*>(ctx)->alloc(&p, bytes) == REMOE_OK ? p : nullptr;
+    };
+    ST_TRY(remoe::tc_seed_build(&h->seed_store, h->x, h->xnorm, c.n_local, c.dim, st, al, h));
+    remoe::TcSeed& sd = h->seed_store;
+    if (sd.n_seg > 0) {
+      const int slabs = mb / 64 + 2;
+      ST_TRY(h->alloc((void**)&sd.keys, (size_t)mb * 2 * std::max(1, h->grid_tc) * 8));
+      ST_TRY(h->alloc((void**)&sd.sync, (size_t)2 * slabs * sizeof(unsigned)));
+      CUDA_TRY(cudaMemsetAsync(sd.sync, 0, (size_t)2 * slabs * sizeof(unsigned), st));
+      if (const char* e = getenv("REMOE_SEED_WAIT_US")) sd.wait_ns = 1000LL * std::max(0, atoi(e));
+    }
+  }
   if (const char* e = getenv("REMOE_SEED")) h->seed_mode = atoi(e) != 0 ? 1 : 0;
+  if (const char* e = getenv("REMOE_SEED_INKERNEL")) h->seed_inkernel = atoi(e) != 0;
   if (const char* e = getenv("REMOE_SEED_MIN_B")) h->seed_min_b = atoi(e);
   if (const char* e = getenv("REMOE_SEED_KS")) h->seed_ks = std::max(0, std::min(32, atoi(e)));
   if (const char* e = getenv("REMOE_PAIR_MIN_B")) h->pair_min_b = atoi(e);
   if (const char* e = getenv("REMOE_NO_GRAPH")) h->use_graphs = atoi(e) == 0;
+  if (h->tc.kn.trace || h->tc.kn.stats) h->use_graphs = false;  // debug knobs read back and print per launch
   if (const char* e = getenv("REMOE_XCHG_AG_MAX")) h->xchg_ag_max = (size_t)std::max(0LL, atoll(e));
   ST_TRY(h->alloc((void**)&h->cand_buf, cand_lanes * capmax * 8));
   ST_TRY(h->alloc((void**)&h->lists, (size_t)mb * lists_max * c.max_k * 8));
@@ -649,7 +670,27 @@ static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k,
     int ks_auto = remoe::seed_ks_for(k);
     while (ks_auto < 32 && (int64_t)lists_min * ks_auto < 4 * k) ks_auto *= 2;
     const int ks = h->seed_ks > 0 ? std::min(h->seed_ks, k) : std::min(ks_auto, k);
-    if (sd && seed && 8 * k <= sd->rows && (int64_t)lists_min * ks >= k) {
+    // the tensor-core scan seeds inside the kernel (TcSeed): the first tiles of the sample
+    // prefix with stride ~1024 / k, each state's h-th best key, threshold = the r-th largest
+    remoe::TcSeedUse su;
+    const remoe::TcSeed& ss = h->seed_store;
+    if (which == 2 && seed && ss.n_seg > 0 && h->seed_inkernel) {
+      int stride = 64, nseg = 1;
+      while (stride > 8 && stride * k > 1024) { stride /= 2; ++nseg; }
+      nseg = std::min(nseg, ss.n_seg);
+      const int hmax = k <= 32 ? 4 : 8;
+      int hh = 1;
+      const int ntl = ss.seg_t0[nseg];
+      while (hh < hmax && ((k + hh - 1) / hh > 32 || ntl < 2 * ((k + hh - 1) / hh))) hh *= 2;
+      const int rr = (k + hh - 1) / hh;
+      if (rr <= 32 && ntl >= 2 * rr) {
+        su.store = &ss;
+        su.n_stiles = ntl;
+        su.h = hh;
+        su.r = rr;
+      }
+    }
+    if ((which == 3 || !su.store) && sd && seed && 8 * k <= sd->rows && (int64_t)lists_min * ks >= k) {
       // Scan the sample with a short register top-k (k_s keys per state, k_s = 1 for
       // k <= 32: a running max, no insertion work): the k-th best key of the union of the
       // per-CTA lists is a real key of the store, hence a lower bound of the final k-th
@@ -673,7 +714,7 @@ static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k,
         which == 3 ? remoe::tc_pair_scan(&h->tc, q, h->qnorm, bc, k, c.sigma, h->xnorm, c.n_local, c.global_offset,
                                          1, h->cand_buf, h->gthr, h->lists, st, &nl, &grid)
                    : remoe::tc_scan(&h->tc, q, h->qnorm, bc, k, c.sigma, h->xnorm, c.n_local, c.global_offset,
-                                    1, h->cand_buf, h->gthr, h->lists, st, &nl, &grid);
+                                    1, h->cand_buf, h->gthr, h->lists, st, &nl, &grid, su.store ? &su : nullptr);
     if (ts != REMOE_OK)
       return fail(ts, "tensor-core scan launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     *launches += nl;
@@ -913,8 +954,8 @@ extern "C" {
 
 remoe_status_t remoe_sps_query(remoe_sps_t h, const uint16_t* q, int32_t B, int32_t k,
                                int64_t* ids, float* scores, float* pred, void* stream) {
+  if (h && h->group) return fail(REMOE_ERR_STATE, "a loopback group member is queried with remoe_sps_query_group");
   ST_TRY(check_query(h, q, B, k, ids, scores, pred));
-  if (h->group) return fail(REMOE_ERR_STATE, "a loopback group member is queried with remoe_sps_query_group");
   if (B == 0) return REMOE_OK;
   DeviceGuard dg(h->cfg.device);
   NvtxRange nr("remoe_sps_query");
@@ -1062,8 +1103,8 @@ static remoe_status_t query_host_graph(remoe_sps* h, const uint16_t* q, int B, i
 remoe_status_t remoe_sps_query_host(remoe_sps_t h, const uint16_t* q, int32_t B, int32_t k,
                                     int64_t* ids, float* scores, float* pred, void* stream) {
   if (!h) return fail(REMOE_ERR_STATE, "handle is NULL");
-  ST_TRY(check_query(h, q, B, k, ids, scores, pred, false));  // host buffers: staged, any alignment
   if (h->group) return fail(REMOE_ERR_STATE, "a loopback group member is queried with remoe_sps_query_group");
+  ST_TRY(check_query(h, q, B, k, ids, scores, pred, false));  // host buffers: staged, any alignment
   if (B == 0) return REMOE_OK;
   DeviceGuard dg(h->cfg.device);
   NvtxRange nr("remoe_sps_query_host");

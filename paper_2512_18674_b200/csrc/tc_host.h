@@ -77,6 +77,29 @@ struct TcPlan {
   unsigned long long* trace_buf = nullptr;
 };
 
+// In-kernel threshold seeding (k_scan_tc): a tiled copy of every s-th store
+// row (s = 64, 32, 16, 8 are prefixes of 1..4 segments), built once per handle.
+struct TcSeed {
+  int n_seg = 0;
+  int seg_t0[5] = {0, 0, 0, 0, 0};   // first sample tile of segment g; seg_t0[n_seg] = tiles
+  int64_t seg_count[4] = {0, 0, 0, 0}, seg_off[4] = {0, 0, 0, 0}, seg_stride[4] = {0, 0, 0, 0};
+  uint16_t* xt = nullptr;            // tiled sample [tiles][D/64][16 KB]
+  float* xn = nullptr;               // its norms [tiles * 128] (padding rows: 1)
+  uint64_t* keys = nullptr;          // [max_batch][2 * grid] published keys
+  unsigned* sync = nullptr;          // [2 * slabs]: arrival count, generation (zeroed at build)
+  long long wait_ns = 100000;        // REMOE_SEED_WAIT_US
+};
+// One scan's use of the sample: the first n_stiles tiles; every state publishes its h-th
+// best sample key and the threshold is the r-th largest published key minus one.
+struct TcSeedUse {
+  const TcSeed* store = nullptr;
+  int n_stiles = 0, h = 1, r = 1;
+};
+// Builds the sample from x / xnorm (device) with `alloc(actx, bytes)` (returns nullptr on
+// failure; the caller owns the memory).  Synchronous on st.
+remoe_status_t tc_seed_build(TcSeed* sd, const uint16_t* x, const float* xnorm, int64_t n_rows, int dim,
+                             cudaStream_t st, void* (*alloc)(void*, size_t), void* actx);
+
 // Writes the tiled, pre-swizzled copy of x [n_rows x dim] (dim % 64 == 0) into xt
 // [ceil(n_rows/128) * 128 * dim] (rows past n_rows are zero).
 cudaError_t tc_tile_store(const uint16_t* x, int64_t n_rows, int dim, uint16_t* xt, cudaStream_t st);
@@ -97,7 +120,7 @@ void tc_plan_destroy(TcPlan* t);
 remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc, int k, float sigma,
                        const float* xnorm, int64_t n_rows, int64_t gid_offset, int64_t gid_stride,
                        uint64_t* cand_buf, unsigned long long* gthr, uint64_t* lists, cudaStream_t st,
-                       int* launches, int* lists_per_query);
+                       int* launches, int* lists_per_query, const TcSeedUse* seed = nullptr);
 // Large batches: the CTA-pair (cta_group::2) GEMM-tiled scan (k_scan_pair.cu), same
 // output contract as tc_scan; 256 queries per pair.
 bool tc_pair_usable(const TcPlan* t);

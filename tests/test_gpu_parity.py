@@ -203,20 +203,22 @@ def test_degenerate_rows(kern):
     assert_parity(compare(q, x, a, 5, ids, sc, pred))
 
 
-def test_dims_and_table_shapes():
-    """D at the minimum (8), odd chunk counts (D=40, 776), D=4096, E=1 and E=256."""
+@pytest.mark.parametrize("B", [6, 9])
+def test_dims_and_table_shapes(B):
+    """D at the minimum (8), odd chunk counts (D=40, 776), D=4096 (streaming kernel only;
+    B = 9 takes its 8-query slab, which must be sized to fit shared memory), E=1 and E=256."""
     rng = np.random.default_rng(4)
     for D, L, E, n in [(8, 3, 1, 777), (40, 2, 256, 3000), (776, 27, 64, 5000), (4096, 4, 8, 2000)]:
         x = gen.f32_to_bf16_bits(rng.standard_normal((n, D)).astype(np.float32))
         a = rng.random((n, L, E)).astype(np.float32) + 1e-3
         a /= a.sum(-1, keepdims=True)
-        q = gen.f32_to_bf16_bits(rng.standard_normal((6, D)).astype(np.float32))
+        q = gen.f32_to_bf16_bits(rng.standard_normal((B, D)).astype(np.float32))
         s = make(x, a, max_k=32)
         for kern in ("stream", "tc", "pair"):
             if not kernel_available(s, kern):
                 continue
             ids, sc, pred = run(s, q, 9)
-            assert_parity(compare(q, x, a, 9, ids, sc, pred))
+            assert_parity(compare(q, x, a, 9, ids, sc, pred), f"D={D} E={E} B={B} {kern}")
         s.close()
 
 
@@ -241,6 +243,11 @@ def test_errors():
         s2.query(q, 5)         # k > N
     ids, sc, pred = s.query(q[:0], 3)  # B == 0: no-op
     assert ids.shape == (0, 3)
+    # a query view 2 bytes off a 16-byte boundary: rejected synchronously, not a fault
+    qm = torch.zeros(2 * c.dim + 8, dtype=torch.int16, device="cuda")[1:1 + 2 * c.dim].view(2, c.dim)
+    with pytest.raises(remoe.RemoeError, match="misaligned"):
+        s.query(qm, 3)
+    s.sync()
     bad = x.copy()
     bad[5, 3] = 0x7FC0       # NaN
     with pytest.raises(remoe.RemoeError, match="INVALID_ARG"):

@@ -37,6 +37,15 @@ def test_js_kernel_matches_oracle():
     Q = torch.tensor([[[0.5, 0.5]], [[0.0, 1.0]], [[0.9, 0.1]]], device="cuda")
     out = remoe.js_divergence(P, Q).cpu().numpy()
     np.testing.assert_allclose(out, [0.0, 1.0, 0.146793], atol=2e-6)
+    # many layers: the per-layer values need > 48 KB of shared memory (L = 20,000 x 4 B)
+    L = 20_000
+    p = np.full((2, L, 2), 0.5, np.float32)
+    q = np.zeros((2, L, 2), np.float32)
+    q[0, :, 0] = 1.0          # [.5,.5] vs [1,0] on every layer
+    q[1] = 0.5                # identical
+    out = remoe.js_divergence(torch.from_numpy(p).cuda(), torch.from_numpy(q).cuda()).cpu().numpy()
+    ref = oracle.js_divergence(p[0, :1], q[0, :1])
+    np.testing.assert_allclose(out, [ref, 0.0], atol=1e-4)  # fp32 sum of 20,000 layer values
 
 
 def test_sps_beats_dop_beats_ef():
