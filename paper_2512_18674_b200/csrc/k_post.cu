@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
                                                uint64_t* __restrict__ out,
                                                unsigned long long* __restrict__ set_thr,
                                                const unsigned long long* __restrict__ lower,
-                                               FinalizeArgs fin) {
+                                               FinalizeArgs fin, unsigned* __restrict__ bump) {
   __shared__ uint64_t cand[kSelCap];
   __shared__ uint64_t topk[256];
   __shared__ unsigned hist[256];
@@ -92,6 +92,9 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int b = blockIdx.x;
   pdl_wait();  // the scan's lists and thresholds
+  // the scan is complete: a new seeding epoch for the next chunk (stale published keys of
+  // this one can never be taken for the next one's)
+  if (bump && b == 0 && t == 0) atomicAdd(bump, 1u);
   const uint64_t* base = in + (int64_t)b * qstride;
   const int nch = (list_len + 31) >> 5;
   const int items = n_lists * nch;
@@ -266,7 +269,8 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
 
 cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride, int64_t lstride,
                          int k, uint64_t* out, cudaStream_t st, unsigned long long* set_thr,
-                         const unsigned long long* lower, const FinalizeArgs* fin, int list_len) {
+                         const unsigned long long* lower, const FinalizeArgs* fin, int list_len,
+                         unsigned* bump) {
   if (B <= 0) return cudaSuccess;
   if (k > 256) return cudaErrorInvalidValue;
   if (list_len <= 0) list_len = k;
@@ -275,7 +279,7 @@ cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride
   cudaError_t e = set_smem_attrs_once((const void*)k_merge, 0);
   if (e != cudaSuccess) return e;
   return launch_pdl(k_merge, dim3(B), dim3(256), 0, st, in, n_lists, qstride, lstride, list_len, k, out, set_thr,
-                    lower, f);
+                    lower, f, bump);
 }
 
 // ---------------------------------------------------------------- S6 + S7

@@ -40,12 +40,13 @@ namespace {
 constexpr int kTileN = 128;          // store rows per tile (UMMA N)
 constexpr int kBlockK = 64;          // bf16 elements per 128-byte swizzle row
 constexpr int kStageBytes = kTileN * kBlockK * 2;  // 16 KB
-constexpr int kThreads = 320;        // 10 warps: TMA, MMA, 8 epilogue
+constexpr int kThreads = 352;        // 11 warps: TMA, MMA, 8 epilogue, seeding
+constexpr int kSeedWarp = 10;        // computes the seeded thresholds (idle without seeding)
 constexpr int kEpiWarps = 8;
 constexpr int kAcc = 4;              // TMEM accumulator stages
 constexpr int kTmemCols = kAcc * kTileN;
 constexpr int kMaxSmem = 232448;     // 227 KB opt-in
-constexpr int kMaxStages = 8;        // stage ring depth cap (deeper rings measured no faster)
+constexpr int kMaxStages = 12;       // stage ring depth cap (TcKnobs::max_stages may lower it)
 
 struct TcArgs {
   const float* xnorm;
@@ -75,10 +76,12 @@ struct TcArgs {
   unsigned long long* stats;  // REMOE_TC_STATS: [0] candidate columns, [1] inserts, [2] chunks with a candidate
   // ---- in-kernel threshold seeding (DESIGN.md §7 "threshold seeding"): each CTA first
   // scans its share of the sample tiles (a tiled copy of every s-th store row, TcSeed)
-  // with a small register tracker per state, publishes the state's h-th best sample key,
-  // and the last CTA of the slab to arrive sets every query's shared threshold to
+  // with a small register tracker per state and publishes the state's h-th best sample
+  // key, tagged with this launch's epoch; the seeding warp of CTA c then waits for every
+  // state's key of the queries m = c (mod grid.x) and raises their shared thresholds to
   // (the r-th largest published key) - 1, r * h >= k: at least k real keys of the store
   // are >= that key, so it is a lower bound of the final k-th best (strict after -1).
+  // The epilogue never waits for it: the thresholds are read again every tile.
   const uint16_t* seed_xt;   // tiled sample (nullptr: no seeding)
   const float* seed_xn;      // sample norms [n tiles * 128]
   int seed_n_stiles;         // sample tiles scanned (a prefix of the segments)
@@ -89,8 +92,10 @@ struct TcArgs {
   int64_t seed_stride[4];
   int seed_h, seed_r;
   uint64_t* seed_keys;       // [nq][2 * gridDim.x] published h-th keys (this launch's queries)
-  unsigned* seed_sync;       // [2 * gridDim.y]: per slab arrival count, generation
-  long long seed_wait_ns;    // how long a CTA waits for the seeded thresholds (0: no wait)
+  unsigned* seed_tags;       // [nq][2 * gridDim.x] epoch of each published key
+  unsigned* seed_done;       // [nq] epoch once the query's seeded threshold is set
+  const unsigned* seed_epoch;  // the epoch of this query chunk (bumped by its merge kernel)
+  long long seed_wait_ns;    // how long the seeding warp waits for all keys (then: the subset)
 };
 }  // namespace
 
@@ -137,7 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = bars + 2 * NST + kAcc;
   uint64_t* cempty = bars + 2 * NST + 2 * kAcc;  // [NST] cluster-wide "slot free" (leader CTA)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NST + 2 * kAcc);
-  volatile int& s_seed_last = *reinterpret_cast<int*>(bars + 3 * NST + 2 * kAcc + 1);  // free slot before sXn
+  volatile unsigned& s_epoch = *reinterpret_cast<unsigned*>(bars + 3 * NST + 2 * kAcc + 1);  // free slot before sXn
   // [2 parities][2 buffers][128] tile x-norms, shared by the 4 warps of a parity
   float* sXn = reinterpret_cast<float*>(bars + ((3 * NST + 2 * kAcc + 2 + 1) & ~1));
   // [M] per-query threshold shared by the two parity states of the CTA (register top-k)
@@ -157,6 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     return (int64_t)blockIdx.x + (i < ns_cta ? i : i - ns_cta) * (int64_t)gridDim.x;
   };
   TRACE(0);
+  if (p.trace && threadIdx.x == 0) p.trace[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + 11] = clock64();
   pdl_trigger();  // the merge kernel may be scheduled as SMs free up
   // Query slab of this CTA (blockIdx.y).  With several slabs, the CTAs of every slab walk
   // the store tiles in the same order (tile = blockIdx.x + j * gridDim.x), so the slabs
@@ -187,6 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < kAcc; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
     for (int s = 0; s < M; ++s) pair_thr[s] = 0ull;
+    if (seeding) s_epoch = *reinterpret_cast<const volatile unsigned*>(p.seed_epoch);
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_x) : "memory");
   }
@@ -223,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("bar.sync 1, %0;" ::"n"(kThreads - 32) : "memory");  // warps 1-9 only
+    asm volatile("bar.sync 1, %0;" ::"n"(kThreads - 32) : "memory");  // warps 1-10 only
     TRACE(2);
   }
 
@@ -239,6 +246,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = it % NST;
           const uint32_t ph = (uint32_t)(it / NST) & 1u;
           mbar_wait(&empty[s], ph ^ 1u);  // this CTA's MMA is done with the slot
+          if (p.dbg & 32) {  // debug (REMOE_TC_DBG bit 32): no load, the slot is "full" at once (wrong results)
+            mbar_arrive(&full[s]);
+            continue;
+          }
           mbar_arrive_expect_tx(&full[s], kStageBytes);
           // tiled store / sample: box (t, kb) is 16 KB contiguous in HBM, already in the
           // swizzled UMMA layout, so a 1-D bulk copy streams it (no 128 B-per-row pattern)
@@ -288,15 +299,79 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive(&empty[s]);
             continue;
           }
-#pragma unroll
-          for (int kk = 0; kk < kBlockK / 16; ++kk)
+          // (debug REMOE_TC_DBG bit 8: 2 of the 4 MMAs per K-block; bit 16: free the slot on
+          // issue instead of on completion -- both give wrong results, timing experiments only)
+          const int nkk = (p.dbg & 8) ? 2 : kBlockK / 16;
+#pragma unroll 4
+          for (int kk = 0; kk < nkk; ++kk)
             umma_bf16(d_tmem, umma_desc(abase + kk * 32), umma_desc(bbase + kk * 32), idesc,
                       (j | kk) != 0);
-          umma_commit(&empty[s]);
+          if (p.dbg & 16) mbar_arrive(&empty[s]);
+          else umma_commit(&empty[s]);
           if (C > 1) umma_commit_mc(&cempty[s], 1);  // the leader's slot-free barrier
         }
         umma_commit(&tfull[acc]);
         if (i == 0) TRACE(5);
+      }
+    }
+  } else if (warp == kSeedWarp) {
+    // ------------------------------------------------ seeding warp
+    // For the queries m = blockIdx.x (mod grid.x) of this slab: wait until every state of
+    // every CTA has published its sample key for m with this launch's epoch (bounded: on a
+    // timeout the keys published so far are used -- the r-th largest of any subset of
+    // published keys is still a lower bound), take the r-th largest key T, raise the
+    // query's shared threshold to T - 1.  Keys are distinct (each sample row belongs to one
+    // state) or 0 (no key).
+    if (seeding) {
+      pdl_wait();  // k_norms zeroes the shared thresholds first
+      const int G2 = 2 * (int)gridDim.x;
+      const unsigned ep = s_epoch;
+      for (int mm = blockIdx.x; mm < nq; mm += gridDim.x) {
+        const size_t base = (size_t)(slab * M + mm) * G2;
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        unsigned ready = 0;  // bit u: slot lane + 32 u has this epoch's key
+        for (;;) {
+#pragma unroll
+          for (int u = 0; u < 10; ++u) {
+            const int idx = lane + 32 * u;
+            if (idx < G2 && !((ready >> u) & 1u)) {
+              unsigned tg;
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(tg) : "l"(p.seed_tags + base + idx) : "memory");
+              if (tg == ep) ready |= 1u << u;
+            } else if (idx >= G2) {
+              ready |= 1u << u;
+            }
+          }
+          if (__all_sync(kFull, ready == 0x3FFu)) break;
+          unsigned long long t1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+          if ((long long)(t1 - t0) > p.seed_wait_ns) break;
+          __nanosleep(128);
+        }
+        uint64_t v[10];
+#pragma unroll
+        for (int u = 0; u < 10; ++u) {
+          const int idx = lane + 32 * u;
+          v[u] = (idx < G2 && ((ready >> u) & 1u)) ? __ldcg(p.seed_keys + base + idx) : 0ull;
+        }
+        uint64_t T = 0;
+        for (int r = 0; r < p.seed_r; ++r) {  // iterative extraction of the maximum
+          uint64_t mx = v[0];
+#pragma unroll
+          for (int u = 1; u < 10; ++u) mx = umax64(mx, v[u]);
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) mx = umax64(mx, __shfl_xor_sync(kFull, mx, off));
+          T = mx;
+          if (T == 0) break;
+#pragma unroll
+          for (int u = 0; u < 10; ++u) v[u] = v[u] == T ? 0ull : v[u];
+        }
+        if (lane == 0) {
+          if (T != 0) atomicMax(gthr_sl + mm, (unsigned long long)(T - 1));
+          __threadfence();
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.seed_done + slab * M + mm), "r"(ep) : "memory");
+        }
       }
     }
   } else {
@@ -384,66 +459,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       return x;
     };
-    // Seeding hand-off, once per thread, before its first store tile: publish the state's
-    // h-th best sample key; the last CTA of the slab to arrive computes every query's
-    // seeded threshold, the others wait for it (bounded: a CTA that times out goes on
-    // with its own thresholds, which is always exact, and picks the seeded ones up later).
-    auto seed_sync = [&](uint64_t kh) {
-      const int G2 = 2 * (int)gridDim.x;
-      if (active) p.seed_keys[(size_t)(slab * M + m) * G2 + 2 * blockIdx.x + parity] = kh;
+    // Seeding hand-off, once per state, before its first store tile (or at the end when it
+    // has none): publish the state's h-th best sample key with this launch's epoch.
+    auto seed_publish = [&](uint64_t kh) {
+      if (!active) return;
+      const size_t slot = (size_t)(slab * M + m) * (2 * gridDim.x) + 2 * blockIdx.x + parity;
+      p.seed_keys[slot] = kh;
       __threadfence();
-      asm volatile("bar.sync 10, %0;" ::"n"(kEpiWarps * 32) : "memory");
-      unsigned* cnt = p.seed_sync + 2 * slab;
-      unsigned gen0 = 0;
-      if (e == 0 && lane == 0) {
-        gen0 = *reinterpret_cast<volatile unsigned*>(cnt + 1);
-        __threadfence();
-        s_seed_last = atomicAdd(cnt, 1u) == gridDim.x - 1u;
-      }
-      asm volatile("bar.sync 10, %0;" ::"n"(kEpiWarps * 32) : "memory");
-      if (s_seed_last) {
-        __threadfence();
-        // r-th largest of the 2 * grid.x published keys of each query: warp e takes queries
-        // e, e + 8, ...; iterative extraction of the maximum (keys are distinct or 0)
-        for (int mm = e; mm < nq; mm += kEpiWarps) {
-          const uint64_t* kp = p.seed_keys + (size_t)(slab * M + mm) * G2;
-          uint64_t v[10];
-#pragma unroll
-          for (int u = 0; u < 10; ++u) v[u] = lane + 32 * u < G2 ? __ldcg(kp + lane + 32 * u) : 0ull;
-          uint64_t T = 0;
-          for (int r = 0; r < p.seed_r; ++r) {
-            uint64_t mx = v[0];
-#pragma unroll
-            for (int u = 1; u < 10; ++u) mx = umax64(mx, v[u]);
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) mx = umax64(mx, __shfl_xor_sync(kFull, mx, off));
-            T = mx;
-            if (T == 0) break;
-#pragma unroll
-            for (int u = 0; u < 10; ++u) v[u] = v[u] == T ? 0ull : v[u];
-          }
-          if (T != 0 && lane == 0) atomicMax(gthr_sl + mm, (unsigned long long)(T - 1));
-        }
-        __threadfence();
-        asm volatile("bar.sync 10, %0;" ::"n"(kEpiWarps * 32) : "memory");
-        if (e == 0 && lane == 0) {
-          *reinterpret_cast<volatile unsigned*>(cnt) = 0u;
-          __threadfence();
-          atomicAdd(cnt + 1, 1u);
-        }
-      } else if (p.seed_wait_ns > 0) {
-        if (e == 0 && lane == 0) {
-          unsigned long long t0, t1;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-          while (*reinterpret_cast<volatile unsigned*>(cnt + 1) == gen0) {
-            __nanosleep(256);
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-            if ((long long)(t1 - t0) > p.seed_wait_ns) break;
-          }
-          __threadfence();
-        }
-        asm volatile("bar.sync 10, %0;" ::"n"(kEpiWarps * 32) : "memory");
-      }
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.seed_tags + slot), "r"(s_epoch) : "memory");
     };
     bool synced = !seeding;
     float4 xv_next = load_xn(parity);
@@ -453,9 +476,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool smp = i < ns_cta;
       if (!smp && !synced) {
         TRACE(3);
-        seed_sync(tracker_key(tr, p.seed_h));
-        TRACE(10);
+        seed_publish(tracker_key(tr, p.seed_h));
         synced = true;
+        // wait (bounded) for this query's seeded threshold: the TMA producer and the MMA run
+        // on meanwhile (four accumulators of slack), and the first store tiles are then
+        // filtered by the seed instead of inserting from an empty list
+        if (active) {
+          unsigned long long t0, t1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          for (;;) {
+            unsigned dn;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(dn) : "l"(p.seed_done + slab * M + m) : "memory");
+            if (dn == s_epoch) break;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if ((long long)(t1 - t0) > p.seed_wait_ns) break;
+            __nanosleep(256);
+          }
+        }
+        TRACE(10);
         gt_next = tk.peek_shared();
       }
       const int acc = (int)(i % kAcc);
@@ -608,7 +646,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if constexpr (KR > 0) tk.publish();
     }
-    if (!synced) seed_sync(tracker_key(tr, p.seed_h));  // this parity had no store tile: still takes part once
+    if (!synced) seed_publish(tracker_key(tr, p.seed_h));  // this parity had no store tile
     TRACE(8);
     if (KR > 0 && p.merge_in_cta) {
       // Merge the two parity states of each query inside the CTA (one list per CTA per
@@ -639,6 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
   TRACE(9);
+  if (p.trace && threadIdx.x == 0) p.trace[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + 12] = clock64();
   if (C > 1) {  // no CTA leaves while a peer may still arrive on its barriers
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
@@ -753,6 +792,9 @@ int dyn_smem_pad() {
   return pad;
 }
 
+// REMOE_TC_MAX_STAGES (read at plan creation): cap of the stage ring depth.
+static int g_max_stages = 0;
+
 // slab_rows: query rows stored per K-block (M for a full slab).
 static size_t tc_smem(int M, int slab_rows, int D, int nst, int buf_bytes) {
   return (size_t)dyn_smem_pad() + (size_t)(D / kBlockK) * slab_rows * 128 + (size_t)nst * kStageBytes +
@@ -762,7 +804,8 @@ static size_t tc_smem(int M, int slab_rows, int D, int nst, int buf_bytes) {
 static int tc_stages(int M, int D, int buf_bytes, int slab_rows = 0) {
   const long avail = (long)kMaxSmem - (long)tc_smem(M, slab_rows > 0 ? slab_rows : M, D, 0, buf_bytes);
   const long n = avail / (kStageBytes + 16);
-  return (int)(n > kMaxStages ? kMaxStages : n);
+  const int cap = g_max_stages > 0 ? g_max_stages : kMaxStages;
+  return (int)(n > cap ? cap : n);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -792,6 +835,7 @@ remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int 
     return REMOE_OK;
   }
   t->kn = TcKnobs::from_env();
+  if (const char* e = getenv("REMOE_TC_MAX_STAGES")) g_max_stages = atoi(e);
   const cuuint64_t gdim[2] = {(cuuint64_t)dim, (cuuint64_t)n_rows};
   const cuuint64_t gstride[1] = {(cuuint64_t)row_stride * 2};
   const cuuint32_t box[2] = {(cuuint32_t)kBlockK, (cuuint32_t)kTileN};
@@ -917,7 +961,7 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
     a.kb_order = kn.kb_order;
     a.slab_rows = SR;
     a.dbg = kn.dbg;
-    if (seed && t->xt && 2 * ctas_per_slab <= 320) {
+    if (seed && t->xt && 2 * ctas_per_slab <= 320 && seed->store->keys && seed->store->tags && seed->store->done) {
       const TcSeed& sd = *seed->store;
       a.seed_xt = sd.xt;
       a.seed_xn = sd.xn;
@@ -932,7 +976,9 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
       a.seed_h = seed->h;
       a.seed_r = seed->r;
       a.seed_keys = sd.keys + (size_t)s0 * 2 * ctas_per_slab;
-      a.seed_sync = sd.sync + 2 * sl0;
+      a.seed_tags = sd.tags + (size_t)s0 * 2 * ctas_per_slab;
+      a.seed_done = sd.done + s0;
+      a.seed_epoch = sd.epoch;
       a.seed_wait_ns = sd.wait_ns;
     }
     if (kn.stats) {  // debug counters (this plan's buffer)
@@ -959,6 +1005,14 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
               a.nq, k, (long long)((n_rows + kTileN - 1) / kTileN));
       const char* names[11] = {"start", "setup", "slab", "seed sync in", "mma first full", "mma tile0 commit",
                                "epi pdl_wait", "epi first tfull", "epi loop done", "end", "seed sync out"};
+      {  // effective SM clock over the CTA's lifetime: clock64 ticks / globaltimer ns
+        double f = 0; int nf = 0;
+        for (int c = 0; c < n_cta; ++c)
+          if (h[c * 16 + 9] > h[c * 16] && h[c * 16 + 12] > h[c * 16 + 11]) {
+            f += (double)(h[c * 16 + 12] - h[c * 16 + 11]) / (double)(h[c * 16 + 9] - h[c * 16]); ++nf;
+          }
+        fprintf(stderr, "  effective SM clock %.0f MHz (mean over %d CTAs)\n", nf ? 1e3 * f / nf : 0.0, nf);
+      }
       for (int i = 0; i < 11; ++i) {
         unsigned long long mx = 0;
         for (int c = 0; c < n_cta; ++c) if (h[c * 16 + i] > mx) mx = h[c * 16 + i];

@@ -155,6 +155,7 @@ struct remoe_sps {
   // the tensor-core scan seeds inside the kernel from a tiled sample (TcSeed, k_scan_tc)
   remoe::TcSeed seed_store{};
   bool seed_inkernel = true;  // REMOE_SEED_INKERNEL=0: the separate seed-scan launch instead (A/B)
+  int seed_segs = 0;          // REMOE_SEED_SEGS: sample segments used by the in-kernel seed (0: by k)
   uint64_t* seed_top = nullptr;
   // -1 auto: seed when k > 32 or B >= seed_min_b; 1 always (REMOE_SEED=1); 0 never
   // (REMOE_SEED=0).  Without a seed every top-k state (a CTA's rows for one query) starts
@@ -469,15 +470,21 @@ static remoe_status_t build_local(remoe_sps* h, const uint16_t* emb, const float
     ST_TRY(remoe::tc_seed_build(&h->seed_store, h->x, h->xnorm, c.n_local, c.dim, st, al, h));
     remoe::TcSeed& sd = h->seed_store;
     if (sd.n_seg > 0) {
-      const int slabs = mb / 64 + 2;
-      ST_TRY(h->alloc((void**)&sd.keys, (size_t)mb * 2 * std::max(1, h->grid_tc) * 8));
-      ST_TRY(h->alloc((void**)&sd.sync, (size_t)2 * slabs * sizeof(unsigned)));
-      CUDA_TRY(cudaMemsetAsync(sd.sync, 0, (size_t)2 * slabs * sizeof(unsigned), st));
+      const size_t slots = (size_t)mb * 2 * std::max(1, h->grid_tc);
+      ST_TRY(h->alloc((void**)&sd.keys, slots * 8));
+      ST_TRY(h->alloc((void**)&sd.tags, slots * sizeof(unsigned)));
+      ST_TRY(h->alloc((void**)&sd.epoch, sizeof(unsigned)));
+      ST_TRY(h->alloc((void**)&sd.done, (size_t)mb * sizeof(unsigned)));
+      CUDA_TRY(cudaMemsetAsync(sd.tags, 0, slots * sizeof(unsigned), st));
+      CUDA_TRY(cudaMemsetAsync(sd.done, 0, (size_t)mb * sizeof(unsigned), st));
+      static const unsigned one = 1;  // epoch 0 would match the zeroed tags
+      CUDA_TRY(cudaMemcpyAsync(sd.epoch, &one, sizeof one, cudaMemcpyHostToDevice, st));
       if (const char* e = getenv("REMOE_SEED_WAIT_US")) sd.wait_ns = 1000LL * std::max(0, atoi(e));
     }
   }
   if (const char* e = getenv("REMOE_SEED")) h->seed_mode = atoi(e) != 0 ? 1 : 0;
   if (const char* e = getenv("REMOE_SEED_INKERNEL")) h->seed_inkernel = atoi(e) != 0;
+  if (const char* e = getenv("REMOE_SEED_SEGS")) h->seed_segs = std::max(0, std::min(4, atoi(e)));
   if (const char* e = getenv("REMOE_SEED_MIN_B")) h->seed_min_b = atoi(e);
   if (const char* e = getenv("REMOE_SEED_KS")) h->seed_ks = std::max(0, std::min(32, atoi(e)));
   if (const char* e = getenv("REMOE_PAIR_MIN_B")) h->pair_min_b = atoi(e);
@@ -628,6 +635,7 @@ static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k,
   if (which == 3 && !remoe::tc_pair_usable(&h->tc))
     return fail(REMOE_ERR_UNSUPPORTED, "CTA-pair tensor-core scan unavailable for this store");
   int grid = 0;  // sorted key lists per query produced by the scan
+  remoe::TcSeedUse su;  // in-kernel seeding of the tensor-core scan (none: su.store == nullptr)
   CUDA_TRY(h->prof_mark(st, true));
   if (which == 1) {
     grid = h->grid_simt;
@@ -672,11 +680,13 @@ static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k,
     const int ks = h->seed_ks > 0 ? std::min(h->seed_ks, k) : std::min(ks_auto, k);
     // the tensor-core scan seeds inside the kernel (TcSeed): the first tiles of the sample
     // prefix with stride ~1024 / k, each state's h-th best key, threshold = the r-th largest
-    remoe::TcSeedUse su;
     const remoe::TcSeed& ss = h->seed_store;
     if (which == 2 && seed && ss.n_seg > 0 && h->seed_inkernel) {
-      int stride = 64, nseg = 1;
-      while (stride > 8 && stride * k > 1024) { stride /= 2; ++nseg; }
+      // every 64th row for k <= 32, every 32nd above (REMOE_SEED_SEGS overrides: 1..4
+      // segments = every 64th, 32nd, 16th, 8th row); the round-1 stride sweep at k = 128
+      // measured strides 8..32 within 3%, and a denser sample costs its bytes
+      int nseg = k <= 32 ? 1 : 2;
+      if (h->seed_segs > 0) nseg = h->seed_segs;
       nseg = std::min(nseg, ss.n_seg);
       const int hmax = k <= 32 ? 4 : 8;
       int hh = 1;
@@ -725,8 +735,15 @@ static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k,
   // ---- S4 (+ S5..S7 fused when world == 1).  gthr[b] holds a lower bound of the
   // final k-th best key (every published value is some state's own k-th best or a
   // seeded strict bound), so the merge drops every key below it.
-  CUDA_TRY(remoe::launch_merge(h->lists, bc, grid, (int64_t)grid * k, k, k, h->local_top, st, nullptr,
-                               h->gthr, fin));
+  const cudaError_t me = remoe::launch_merge(h->lists, bc, grid, (int64_t)grid * k, k, k, h->local_top, st, nullptr,
+                                             h->gthr, fin, -1, su.store ? h->seed_store.epoch : nullptr);
+  if (me != cudaSuccess && su.store) {
+    // the seeded scan published keys under the current epoch and nothing bumps it now:
+    // retire them so a later chunk cannot read them as its own
+    cudaMemsetAsync(h->seed_store.tags, 0, (size_t)c.max_batch * 2 * std::max(1, h->grid_tc) * sizeof(unsigned), st);
+    cudaMemsetAsync(h->seed_store.done, 0, (size_t)c.max_batch * sizeof(unsigned), st);
+  }
+  CUDA_TRY(me);
   ++*launches;
   return REMOE_OK;
 }

@@ -86,8 +86,10 @@ struct TcSeed {
   uint16_t* xt = nullptr;            // tiled sample [tiles][D/64][16 KB]
   float* xn = nullptr;               // its norms [tiles * 128] (padding rows: 1)
   uint64_t* keys = nullptr;          // [max_batch][2 * grid] published keys
-  unsigned* sync = nullptr;          // [2 * slabs]: arrival count, generation (zeroed at build)
-  long long wait_ns = 100000;        // REMOE_SEED_WAIT_US
+  unsigned* tags = nullptr;          // [max_batch][2 * grid] their epochs (zeroed at build)
+  unsigned* done = nullptr;          // [max_batch] epoch once a query's seeded threshold is set
+  unsigned* epoch = nullptr;         // current epoch (starts at 1; bumped by each chunk's merge)
+  long long wait_ns = 200000;        // REMOE_SEED_WAIT_US: the seeding warp's wait bound
 };
 // One scan's use of the sample: the first n_stiles tiles; every state publishes its h-th
 // best sample key and the threshold is the r-th largest published key minus one.
