@@ -236,83 +236,101 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
-    if (lane == 0) {
-      int it = 0;
-      for (int64_t i = 0; i < n_it; ++i) {
-        const bool smp = i < ns_cta;
-        const int64_t t = tile_of(i);
-        for (int j = 0; j < nkb; ++j, ++it) {
-          const int kb = kb_at(j, nkb, p.kb_order);
-          const int s = it % NST;
-          const uint32_t ph = (uint32_t)(it / NST) & 1u;
-          mbar_wait(&empty[s], ph ^ 1u);  // this CTA's MMA is done with the slot
+    // The whole warp walks the loop (warp-uniform control flow keeps the loop state in
+    // uniform registers); lane 0 issues the copies.
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t i = 0; i < n_it; ++i) {
+      const bool smp = i < ns_cta;
+      const int64_t t = tile_of(i);
+      // tiled store / sample: box (t, kb) is 16 KB contiguous in HBM, already in the swizzled
+      // UMMA layout, so a 1-D bulk copy streams it (no 128 B-per-row DRAM pattern)
+      const uint16_t* tsrc = smp ? p.seed_xt + (size_t)t * nkb * (kStageBytes / 2)
+                                 : p.xt ? p.xt + (size_t)t * nkb * (kStageBytes / 2) : nullptr;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1u);  // this CTA's MMA is done with the slot
+        if (lane == 0) {
           if (p.dbg & 32) {  // debug (REMOE_TC_DBG bit 32): no load, the slot is "full" at once (wrong results)
             mbar_arrive(&full[s]);
-            continue;
-          }
-          mbar_arrive_expect_tx(&full[s], kStageBytes);
-          // tiled store / sample: box (t, kb) is 16 KB contiguous in HBM, already in the
-          // swizzled UMMA layout, so a 1-D bulk copy streams it (no 128 B-per-row pattern)
-          const uint16_t* src = smp ? p.seed_xt + ((size_t)t * nkb + kb) * (kStageBytes / 2)
-                                    : p.xt ? p.xt + ((size_t)t * nkb + kb) * (kStageBytes / 2) : nullptr;
-          if (C == 1) {
-            if (src) bulk_g2s(sB + (size_t)s * kStageBytes, src, kStageBytes, &full[s]);
-            else tma_load_2d(sB + (size_t)s * kStageBytes, &tmap_x, kb * kBlockK, (int)(t * kTileN), &full[s]);
-          } else if (crank == 0) {
-            mbar_wait(&cempty[s], ph ^ 1u);  // every CTA of the cluster is done with the slot
-            if (src)
-              bulk_g2s_mc(sB + (size_t)s * kStageBytes, src, kStageBytes, &full[s], (uint16_t)((1u << C) - 1u));
-            else
-              tma_load_2d_mc(sB + (size_t)s * kStageBytes, &tmap_x, kb * kBlockK, (int)(t * kTileN), &full[s],
-                             (uint16_t)((1u << C) - 1u));
+          } else {
+            mbar_arrive_expect_tx(&full[s], kStageBytes);
+            const uint16_t* src = tsrc ? tsrc + (size_t)kb * (kStageBytes / 2) : nullptr;
+            if (C == 1) {
+              if (src) bulk_g2s(sB + (size_t)s * kStageBytes, src, kStageBytes, &full[s]);
+              else tma_load_2d(sB + (size_t)s * kStageBytes, &tmap_x, kb * kBlockK, (int)(t * kTileN), &full[s]);
+            } else if (crank == 0) {
+              mbar_wait(&cempty[s], ph ^ 1u);  // every CTA of the cluster is done with the slot
+              if (src)
+                bulk_g2s_mc(sB + (size_t)s * kStageBytes, src, kStageBytes, &full[s], (uint16_t)((1u << C) - 1u));
+              else
+                tma_load_2d_mc(sB + (size_t)s * kStageBytes, &tmap_x, kb * kBlockK, (int)(t * kTileN), &full[s],
+                               (uint16_t)((1u << C) - 1u));
+            }
           }
         }
+        __syncwarp();
+        if (++s == NST) { s = 0; ph ^= 1u; }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer (one thread)
-    if (lane == 0) {
-      // kind::f16: D fp32 (bit 4), A bf16 (bits 7-9 = 1), B bf16 (bits 10-12 = 1),
-      // both K-major, N >> 3 at bit 17, M >> 4 at bit 24
-      // (debug REMOE_TC_DBG bit 4: N = 32, a quarter of the MMA work; wrong results)
-      const uint32_t nn = (p.dbg & 4) ? 32u : (uint32_t)kTileN;
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((nn >> 3) << 17) |
-                             ((uint32_t)(M >> 4) << 24);
-      const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
-      int it = 0;
-      for (int64_t i = 0; i < n_it; ++i) {
-        const int acc = (int)(i % kAcc);
-        const uint32_t aph = (uint32_t)(i / kAcc) & 1u;
-        mbar_wait(&tempty[acc], aph ^ 1u);
+    // ------------------------------------------------ MMA issuer
+    // The whole warp walks the loop; lane 0 issues.  The per-K-block work is kept minimal --
+    // descriptors advanced by constants, no division -- because the issuing thread's own
+    // instruction latency, not the tensor pipe, bounded the stream (REMOE_TC_TRACE cycle
+    // split: ~90% of the issuer's time was issue work with an index/division-heavy loop).
+    // kind::f16: D fp32 (bit 4), A bf16 (bits 7-9 = 1), B bf16 (bits 10-12 = 1),
+    // both K-major, N >> 3 at bit 17, M >> 4 at bit 24
+    // (debug REMOE_TC_DBG bit 4: N = 32, a quarter of the MMA work; wrong results)
+    const uint32_t nn = (p.dbg & 4) ? 32u : (uint32_t)kTileN;
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((nn >> 3) << 17) |
+                           ((uint32_t)(M >> 4) << 24);
+    // descriptor = ((address >> 4) & 0x3FFF) | constant bits: offsets add in 16-byte units
+    const uint64_t da0 = umma_desc(smem_u32(sA)), db0 = umma_desc(smem_u32(sB));
+    const uint64_t da_kb = (uint64_t)(SR * 128) >> 4, db_st = (uint64_t)kStageBytes >> 4;
+    const bool skip_mma = (p.dbg & 1) != 0;
+    int s = 0;
+    uint32_t ph = 0;
+    long long w_full = 0, w_tempty = 0, t_loop0 = p.trace ? clock64() : 0;  // REMOE_TC_TRACE cycle split
+    for (int64_t i = 0; i < n_it; ++i) {
+      const int acc = (int)(i & (kAcc - 1));
+      const uint32_t aph = (uint32_t)(i / kAcc) & 1u;
+      long long c0 = p.trace ? clock64() : 0;
+      mbar_wait(&tempty[acc], aph ^ 1u);
+      if (p.trace) w_tempty += clock64() - c0;
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kTileN);
+      uint64_t da = da0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        c0 = p.trace ? clock64() : 0;
+        mbar_wait(&full[s], ph);
+        if (p.trace) w_full += clock64() - c0;
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kTileN);
-        for (int j = 0; j < nkb; ++j, ++it) {
-          const int kb = kb_at(j, nkb, p.kb_order);
-          const int s = it % NST;
-          const uint32_t ph = (uint32_t)(it / NST) & 1u;
-          mbar_wait(&full[s], ph);
-          if (it == 0) TRACE(4);
-          tc_fence_after();
-          const uint32_t abase = a0 + (uint32_t)(kb * SR * 128);
-          const uint32_t bbase = b0 + (uint32_t)(s * kStageBytes);
-          if (p.dbg & 1) {  // debug (REMOE_TC_DBG=1): no MMA, free the slot at once (wrong results)
+        if (lane == 0) {
+          if (skip_mma) {  // debug (REMOE_TC_DBG=1): no MMA, free the slot at once (wrong results)
             mbar_arrive(&empty[s]);
-            continue;
+          } else {
+            const uint64_t db = db0 + (uint64_t)s * db_st;
+            umma_bf16(d_tmem, da, db, idesc, kb != 0);
+            umma_bf16(d_tmem, da + 2, db + 2, idesc, 1);
+            umma_bf16(d_tmem, da + 4, db + 4, idesc, 1);
+            umma_bf16(d_tmem, da + 6, db + 6, idesc, 1);
+            umma_commit(&empty[s]);
+            if (C > 1) umma_commit_mc(&cempty[s], 1);  // the leader's slot-free barrier
           }
-          // (debug REMOE_TC_DBG bit 8: 2 of the 4 MMAs per K-block; bit 16: free the slot on
-          // issue instead of on completion -- both give wrong results, timing experiments only)
-          const int nkk = (p.dbg & 8) ? 2 : kBlockK / 16;
-#pragma unroll 4
-          for (int kk = 0; kk < nkk; ++kk)
-            umma_bf16(d_tmem, umma_desc(abase + kk * 32), umma_desc(bbase + kk * 32), idesc,
-                      (j | kk) != 0);
-          if (p.dbg & 16) mbar_arrive(&empty[s]);
-          else umma_commit(&empty[s]);
-          if (C > 1) umma_commit_mc(&cempty[s], 1);  // the leader's slot-free barrier
         }
-        umma_commit(&tfull[acc]);
-        if (i == 0) TRACE(5);
+        __syncwarp();
+        da += da_kb;
+        if (++s == NST) { s = 0; ph ^= 1u; }
       }
+      if (lane == 0) umma_commit(&tfull[acc]);
+      __syncwarp();
+      if (i == 0) TRACE(5);
+    }
+    if (p.trace && lane == 0) {
+      unsigned long long* tr = p.trace + (blockIdx.y * gridDim.x + blockIdx.x) * 16;
+      tr[13] = (unsigned long long)(clock64() - t_loop0);
+      tr[14] = (unsigned long long)w_full;
+      tr[15] = (unsigned long long)w_tempty;
     }
   } else if (warp == kSeedWarp) {
     // ------------------------------------------------ seeding warp
@@ -1012,6 +1030,10 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
             f += (double)(h[c * 16 + 12] - h[c * 16 + 11]) / (double)(h[c * 16 + 9] - h[c * 16]); ++nf;
           }
         fprintf(stderr, "  effective SM clock %.0f MHz (mean over %d CTAs)\n", nf ? 1e3 * f / nf : 0.0, nf);
+        double lp = 0, wf = 0, wt = 0;
+        for (int c = 0; c < n_cta; ++c) { lp += h[c * 16 + 13]; wf += h[c * 16 + 14]; wt += h[c * 16 + 15]; }
+        fprintf(stderr, "  MMA issuer cycles (mean per CTA): loop %.0f, waiting full %.0f (%.0f%%), waiting tempty %.0f (%.0f%%)\n",
+                lp / n_cta, wf / n_cta, 100 * wf / (lp + 1), wt / n_cta, 100 * wt / (lp + 1));
       }
       for (int i = 0; i < 11; ++i) {
         unsigned long long mx = 0;
