@@ -417,13 +417,11 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
                : "r"(smem_u32(p)));
   return r;
 }
-__device__ __forceinline__ float4 lds128f(const void* p) {
-  float4 r;
-  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-               : "r"(smem_u32(p)));
-  return r;
-}
+// A plain C++ shared-memory load (not volatile asm): the compiler may batch the eight
+// loads of a chunk ahead of the arithmetic; barriers (asm with "memory" clobbers) still
+// order it.  The volatile asm form serialised load -> FMA -> compare chains per column
+// (~100 cycles per column in the seeding pass, REMOE_TC_TRACE cycle counters).
+__device__ __forceinline__ float4 lds128f(const void* p) { return *reinterpret_cast<const float4*>(p); }
 __device__ __forceinline__ uint4 ldg_nc128(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"

@@ -79,8 +79,8 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
                                                int64_t qstride, int64_t lstride, int list_len, int k,
                                                uint64_t* __restrict__ out,
                                                unsigned long long* __restrict__ set_thr,
-                                               const unsigned long long* __restrict__ lower,
-                                               FinalizeArgs fin, unsigned* __restrict__ bump) {
+                                               unsigned long long* __restrict__ lower,
+                                               FinalizeArgs fin, unsigned* __restrict__ bump, int reset_lower) {
   __shared__ uint64_t cand[kSelCap];
   __shared__ uint64_t topk[256];
   __shared__ unsigned hist[256];
@@ -99,6 +99,10 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
   const int nch = (list_len + 31) >> 5;
   const int items = n_lists * nch;
   uint64_t lb = lower ? lower[b] : 0ull;
+  if (lower && reset_lower) {
+    __syncthreads();                 // every thread has read it
+    if (t == 0) lower[b] = 0ull;     // the next chunk's scan starts from no threshold
+  }
   if (lb == 0) lb = 1;  // sentinel keys (0) never count
   auto item_key = [&](int it) -> uint64_t {
     if (it >= items) return 0ull;
@@ -269,8 +273,8 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
 
 cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride, int64_t lstride,
                          int k, uint64_t* out, cudaStream_t st, unsigned long long* set_thr,
-                         const unsigned long long* lower, const FinalizeArgs* fin, int list_len,
-                         unsigned* bump) {
+                         unsigned long long* lower, const FinalizeArgs* fin, int list_len,
+                         unsigned* bump, bool reset_lower) {
   if (B <= 0) return cudaSuccess;
   if (k > 256) return cudaErrorInvalidValue;
   if (list_len <= 0) list_len = k;
@@ -279,7 +283,7 @@ cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride
   cudaError_t e = set_smem_attrs_once((const void*)k_merge, 0);
   if (e != cudaSuccess) return e;
   return launch_pdl(k_merge, dim3(B), dim3(256), 0, st, in, n_lists, qstride, lstride, list_len, k, out, set_thr,
-                    lower, f, bump);
+                    lower, f, bump, reset_lower ? 1 : 0);
 }
 
 // ---------------------------------------------------------------- S6 + S7

@@ -68,7 +68,6 @@ struct PairArgs {
   uint64_t* out;           // lists[(q * lists_per_query + l) * k + i]
   int smem_bufs;
   int merge_in_cta;
-  int kb_order;            // K-block visiting order (kb_at)
 };
 }  // namespace
 
@@ -124,51 +123,58 @@ __global__ void __launch_bounds__(kPThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (both CTAs)
-    if (lane == 0) {
-      const uint32_t full0 = mapa_shared(smem_u32(full), 0);  // the leader's full barriers
-      int it = 0;
-      for (int64_t t = pair; t < n_tiles; t += npairs) {
-        const int xrow = (int)(t * kPairN) + (int)crank * 128;
-        for (int j = 0; j < nkb; ++j, ++it) {
-          const int kb = kb_at(j, nkb, p.kb_order);
-          const int s = it % NST;
-          const uint32_t ph = (uint32_t)(it / NST) & 1u;
-          mbar_wait(&empty[s], ph ^ 1u);  // the pair's MMA is done with this CTA's slot
+    // Warp-uniform loop (loop state in uniform registers), lane 0 issues; no division per
+    // K-block (the issuing thread's instruction latency bounds these loops, k_scan_tc).
+    const uint32_t full0 = mapa_shared(smem_u32(full), 0);  // the leader's full barriers
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = pair; t < n_tiles; t += npairs) {
+      const int xrow = (int)(t * kPairN) + (int)crank * 128;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty[s], ph ^ 1u);  // the pair's MMA is done with this CTA's slot
+        if (lane == 0) {
           if (crank == 0) mbar_arrive_expect_tx(&full[s], 4 * kBox);  // both CTAs' A and B boxes
           tma_load_2d_pair(sA + (size_t)s * kBox, &tmap_q, kb * kPBK, qrow0, full0 + 8u * (uint32_t)s);
           tma_load_2d_pair(sB + (size_t)s * kBox, &tmap_x, kb * kPBK, xrow, full0 + 8u * (uint32_t)s);
         }
+        __syncwarp();
+        if (++s == NST) { s = 0; ph ^= 1u; }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer (leader CTA, one thread)
-    if (crank == 0 && lane == 0) {
+    // ------------------------------------------------ MMA issuer (leader CTA)
+    if (crank == 0) {
       // kind::f16: D fp32 (bit 4), A bf16 (bits 7-9 = 1), B bf16 (bits 10-12 = 1), both
       // K-major, N >> 3 at bit 17, M >> 4 at bit 24 (M = 256: the pair)
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kPairN >> 3) << 17) |
                              ((uint32_t)(256 >> 4) << 24);
-      const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
-      int it = 0, i = 0;
+      const uint64_t da0 = umma_desc(smem_u32(sA)), db0 = umma_desc(smem_u32(sB));
+      const uint64_t dst = (uint64_t)kBox >> 4;  // one stage, in descriptor address units
+      int s = 0;
+      uint32_t ph = 0;
+      int i = 0;
       for (int64_t t = pair; t < n_tiles; t += npairs, ++i) {
         const int acc = i & 1;
         const uint32_t aph = (uint32_t)(i >> 1) & 1u;
         mbar_wait(&tempty[acc], aph ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kPairN);
-        for (int j = 0; j < nkb; ++j, ++it) {
-          const int s = it % NST;
-          const uint32_t ph = (uint32_t)(it / NST) & 1u;
+        for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint32_t abase = a0 + (uint32_t)(s * kBox);
-          const uint32_t bbase = b0 + (uint32_t)(s * kBox);
-#pragma unroll
-          for (int kk = 0; kk < kPBK / 16; ++kk)
-            umma_bf16_pair(d_tmem, umma_desc(abase + kk * 32), umma_desc(bbase + kk * 32), idesc,
-                           (j | kk) != 0);
-          umma_commit_pair(&empty[s], 3);  // frees slot s in both CTAs
+          if (lane == 0) {
+            const uint64_t da = da0 + (uint64_t)s * dst, db = db0 + (uint64_t)s * dst;
+            umma_bf16_pair(d_tmem, da, db, idesc, kb != 0);
+            umma_bf16_pair(d_tmem, da + 2, db + 2, idesc, 1);
+            umma_bf16_pair(d_tmem, da + 4, db + 4, idesc, 1);
+            umma_bf16_pair(d_tmem, da + 6, db + 6, idesc, 1);
+            umma_commit_pair(&empty[s], 3);  // frees slot s in both CTAs
+          }
+          __syncwarp();
+          if (++s == NST) { s = 0; ph ^= 1u; }
         }
-        umma_commit_pair(&tfull[acc], 3);  // accumulator ready in both CTAs
+        if (lane == 0) umma_commit_pair(&tfull[acc], 3);  // accumulator ready in both CTAs
+        __syncwarp();
       }
     }
   } else {
@@ -467,7 +473,6 @@ remoe_status_t tc_pair_scan(TcPlan* t, const uint16_t* q, const float* qnorm, in
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return REMOE_ERR_CUDA;
     PairArgs a{};
-    a.kb_order = t->kn.kb_order;
     a.xnorm = xnorm;
     a.n_rows = n_rows;
     a.gid_offset = gid_offset;

@@ -46,6 +46,7 @@ constexpr int kEpiWarps = 8;
 constexpr int kAcc = 4;              // TMEM accumulator stages
 constexpr int kTmemCols = kAcc * kTileN;
 constexpr int kMaxSmem = 232448;     // 227 KB opt-in
+constexpr int kTraceSlots = 32;     // REMOE_TC_TRACE stamps per CTA
 constexpr int kMaxStages = 12;       // stage ring depth cap (TcKnobs::max_stages may lower it)
 
 struct TcArgs {
@@ -68,7 +69,6 @@ struct TcArgs {
   int cluster;             // CTAs per cluster along y (multicast of the store tiles), 1 = none
   int epi_sleep;           // epilogue waits with a suspend-time hint (REMOE_EPI_SLEEP=1)
   const uint16_t* xt;      // tiled store (TcPlan::xt): 1-D bulk copies, else the tensor map
-  int kb_order;            // K-block visiting order (kb_at)
   int dbg;                 // REMOE_TC_DBG bits (experiments only; 1 = skip the MMA)
   int slab_rows;           // query rows stored per K-block (multiple of 8, <= M): a single
                            // slab of nq queries stores only ceil(nq/8) 8-row atoms
@@ -96,6 +96,7 @@ struct TcArgs {
   unsigned* seed_done;       // [nq] epoch once the query's seeded threshold is set
   const unsigned* seed_epoch;  // the epoch of this query chunk (bumped by its merge kernel)
   long long seed_wait_ns;    // how long the seeding warp waits for all keys (then: the subset)
+  int norms_in_kernel;       // S1 in the prologue (no k_norms launch; qnorm unused)
 };
 }  // namespace
 
@@ -103,24 +104,12 @@ struct TcArgs {
 // lanes 0-15 of each 32-lane TMEM quarter (row r -> lane 32*(r/16) + r%16).  Slab row
 // r = R*q + l (R = M/4 rows per quarter) holds query m = 4*l + q, so a batch smaller than
 // M spreads over all four epilogue quarters instead of filling the first one.
-// The h-th best key of a register tracker (h <= K), by selects (no run-time register index).
-// The list is sorted descending, so the h-th best is the minimum of the first h entries: a
-// min-reduction (a select chain on j == h - 1 gets turned into a dynamic register index,
-// which demotes the whole tracker to the local stack).
-template <int K>
-__device__ __forceinline__ uint64_t tracker_key(const RegTopk<K>& tr, int h) {
-  uint64_t kh = tr.L[0];
-#pragma unroll
-  for (int j = 1; j < K; ++j) kh = umin64(kh, j < h ? tr.L[j] : ~0ull);
-  return kh;
-}
-
 #define TRACE(idx)                                                                              \
   do {                                                                                          \
     if (p.trace && (threadIdx.x & 31) == 0) {                                                   \
       unsigned long long t_;                                                                    \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                    \
-      p.trace[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + (idx)] = t_;                         \
+      p.trace[(blockIdx.y * gridDim.x + blockIdx.x) * kTraceSlots + (idx)] = t_;                         \
     }                                                                                           \
   } while (0)
 
@@ -147,7 +136,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* sXn = reinterpret_cast<float*>(bars + ((3 * NST + 2 * kAcc + 2 + 1) & ~1));
   // [M] per-query threshold shared by the two parity states of the CTA (register top-k)
   unsigned long long* pair_thr = reinterpret_cast<unsigned long long*>(sXn + 4 * kTileN);  // [M]
-  uint64_t* sBuf = reinterpret_cast<uint64_t*>(pair_thr + M);  // [256][CAP] if p.smem_bufs
+  float* sQn = reinterpret_cast<float*>(pair_thr + M);  // [M] query norms (p.norms_in_kernel)
+  uint64_t* sBuf = reinterpret_cast<uint64_t*>(sQn + M);  // [256][CAP] if p.smem_bufs
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -162,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     return (int64_t)blockIdx.x + (i < ns_cta ? i : i - ns_cta) * (int64_t)gridDim.x;
   };
   TRACE(0);
-  if (p.trace && threadIdx.x == 0) p.trace[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + 11] = clock64();
+  if (p.trace && threadIdx.x == 0) p.trace[(blockIdx.y * gridDim.x + blockIdx.x) * kTraceSlots + 11] = clock64();
   pdl_trigger();  // the merge kernel may be scheduled as SMs free up
   // Query slab of this CTA (blockIdx.y).  With several slabs, the CTAs of every slab walk
   // the store tiles in the same order (tile = blockIdx.x + j * gridDim.x), so the slabs
@@ -232,6 +222,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("bar.sync 1, %0;" ::"n"(kThreads - 32) : "memory");  // warps 1-10 only
     TRACE(2);
+  }
+  if (p.norms_in_kernel && warp >= 2 && warp < 2 + kEpiWarps) {
+    // S1 from the resident slab: |q_m| = sqrt(sum_d q_md^2), one warp per query in the
+    // k_norms order (lane partial sums over 16-byte chunks cc = lane, lane + 32, ...;
+    // fixed xor butterfly), so the bits equal launch_norms' on every CTA and position
+    for (int mm = warp - 2; mm < nq; mm += kEpiWarps) {
+      float acc2 = 0.f;
+      for (int cc = lane; cc < (D >> 3); cc += 32) {
+        const int kb = cc >> 3, c = cc & 7;
+        const uint4 w = lds128(sA + (size_t)kb * SR * 128 + mm * 128 + ((c ^ (mm & 7)) << 4));
+        const float vv[8] = {bf_lo(w.x), bf_hi(w.x), bf_lo(w.y), bf_hi(w.y),
+                             bf_lo(w.z), bf_hi(w.z), bf_lo(w.w), bf_hi(w.w)};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc2 = __fmaf_rn(vv[u], vv[u], acc2);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc2 += __shfl_xor_sync(kFull, acc2, off);
+      if (lane == 0) sQn[mm] = __fsqrt_rn(acc2);
+    }
+    asm volatile("bar.sync 11, %0;" ::"n"(kEpiWarps * 32) : "memory");  // the epilogue warps
   }
 
   if (warp == 0) {
@@ -327,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (i == 0) TRACE(5);
     }
     if (p.trace && lane == 0) {
-      unsigned long long* tr = p.trace + (blockIdx.y * gridDim.x + blockIdx.x) * 16;
+      unsigned long long* tr = p.trace + (blockIdx.y * gridDim.x + blockIdx.x) * kTraceSlots;
       tr[13] = (unsigned long long)(clock64() - t_loop0);
       tr[14] = (unsigned long long)w_full;
       tr[15] = (unsigned long long)w_tempty;
@@ -346,45 +356,48 @@ __global__ void __launch_bounds__(kThreads, 1)
       const unsigned ep = s_epoch;
       for (int mm = blockIdx.x; mm < nq; mm += gridDim.x) {
         const size_t base = (size_t)(slab * M + mm) * G2;
-        unsigned long long t0;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        const long long t0 = clock64();  // SM cycle counter: cheap (a %globaltimer read is not)
         unsigned ready = 0;  // bit u: slot lane + 32 u has this epoch's key
         for (;;) {
 #pragma unroll
           for (int u = 0; u < 10; ++u) {
             const int idx = lane + 32 * u;
             if (idx < G2 && !((ready >> u) & 1u)) {
+              // relaxed loads (independent, in flight together); one fence once all are
+              // seen (an acquire per load serialised ten L2 round trips per poll)
               unsigned tg;
-              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(tg) : "l"(p.seed_tags + base + idx) : "memory");
+              asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(tg) : "l"(p.seed_tags + base + idx) : "memory");
               if (tg == ep) ready |= 1u << u;
             } else if (idx >= G2) {
               ready |= 1u << u;
             }
           }
           if (__all_sync(kFull, ready == 0x3FFu)) break;
-          unsigned long long t1;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-          if ((long long)(t1 - t0) > p.seed_wait_ns) break;
+          if (clock64() - t0 > 2 * p.seed_wait_ns) break;  // ~ns at <= 2 GHz
           __nanosleep(128);
         }
-        uint64_t v[10];
+        __threadfence();  // acquire: the keys written before each seen tag
+        // the published keys' score words (key >> 32; 0 = no key)
+        uint32_t hi[10];
 #pragma unroll
         for (int u = 0; u < 10; ++u) {
           const int idx = lane + 32 * u;
-          v[u] = (idx < G2 && ((ready >> u) & 1u)) ? __ldcg(p.seed_keys + base + idx) : 0ull;
+          hi[u] = (idx < G2 && ((ready >> u) & 1u)) ? (uint32_t)(__ldcg(p.seed_keys + base + idx) >> 32) : 0u;
         }
-        uint64_t T = 0;
-        for (int r = 0; r < p.seed_r; ++r) {  // iterative extraction of the maximum
-          uint64_t mx = v[0];
+        // T = the r-th largest score word, by a 32-step radix select with warp-wide counts
+        // (cost independent of r).  At least r published keys -- r distinct real keys of the
+        // store -- are >= T << 32, so T << 32 - 1 is a strict lower bound of the k-th best
+        // (r * h >= k).
+        uint32_t pre = 0;
+#pragma unroll 1
+        for (int b = 31; b >= 0; --b) {
+          const uint32_t cand = pre | (1u << b);
+          int cnt = 0;
 #pragma unroll
-          for (int u = 1; u < 10; ++u) mx = umax64(mx, v[u]);
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) mx = umax64(mx, __shfl_xor_sync(kFull, mx, off));
-          T = mx;
-          if (T == 0) break;
-#pragma unroll
-          for (int u = 0; u < 10; ++u) v[u] = v[u] == T ? 0ull : v[u];
+          for (int u = 0; u < 10; ++u) cnt += hi[u] >= cand ? 1 : 0;
+          if (__reduce_add_sync(kFull, (unsigned)cnt) >= (unsigned)p.seed_r) pre = cand;
         }
+        const uint64_t T = (uint64_t)pre << 32;
         if (lane == 0) {
           if (T != 0) atomicMax(gthr_sl + mm, (unsigned long long)(T - 1));
           __threadfence();
@@ -413,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool active = (M == 128 || lane < 16) && m < nq;
     pdl_wait();  // k_norms: query norms and zeroed shared thresholds
     TRACE(6);
-    const float qn = active ? qnorm_sl[m] : 0.f;
+    const float qn = active ? (p.norms_in_kernel ? sQn[m] : qnorm_sl[m]) : 0.f;
     const int slot = e * 32 + lane;
     // the tile's |x_j|: one copy per parity, double buffered by iteration.  Written after
     // the tile's accumulator wait: by then every warp of the parity has released the
@@ -428,11 +441,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (KR > 0) tk.init(p.k, active ? gthr_sl + m : nullptr);
     else tk.init(buf, active ? gthr_sl + m : nullptr);
     if (!active) tk.tlim = __int_as_float(0x7f800000);  // +inf: never a candidate
-    // seeding tracker: the best kHS keys of this state's sample tiles (h <= kHS of them count)
-    constexpr int kHS = KR > 0 ? 4 : 8;
-    RegTopk<kHS> tr;
-    tr.init(kHS, nullptr);
-    if (!active) tr.tlim = __int_as_float(0x7f800000);
+    // Seeding tracker: the kHS best per-chunk maxima of this state's sample tiles, as (dot,
+    // den, gid) ranked by cross-multiplication (no division, no key, no 64-bit compares);
+    // at the hand-off the exact keys of the first h of them are computed and their minimum
+    // is published: h real keys of this state are >= it, which is all the seed needs (an
+    // fp32 cross-multiplied ranking only makes the published key smaller, never invalid).  The sample
+    // tiles deliberately do NOT feed the real top-k state: from an empty list every column
+    // is an insert (~450 cycles of dependent latency each), ~30 us per 128-row tile.
+    constexpr int kHS = 1;  // h = 1: each state publishes its best sample key (runtime.cu)
+    float tr_dot[kHS], tr_den[kHS];
+    uint32_t tr_gid[kHS];
+#pragma unroll
+    for (int j = 0; j < kHS; ++j) {
+      tr_dot[j] = -__int_as_float(0x7f800000); tr_den[j] = 1.f;
+      tr_gid[j] = 0xFFFFFFFFu;
+    }
+    auto seed_key = [&]() -> uint64_t {
+      uint64_t kmin = ~0ull;
+#pragma unroll
+      for (int j = 0; j < kHS; ++j) {
+        if (j < p.seed_h) {
+          const uint64_t key = tr_gid[j] == 0xFFFFFFFFu ? 0ull : make_key(__fdiv_rn(tr_dot[j], tr_den[j]), (int64_t)tr_gid[j]);
+          kmin = umin64(kmin, key);
+        }
+      }
+      return kmin == ~0ull ? 0ull : kmin;
+    };
 
     // tile i of the sequence: x-norm source, valid rows, global id of column j = gbase + j * gstride
     struct TileInfo { const float* xn; int nvalid; int64_t gbase, gstride; };
@@ -494,23 +528,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool smp = i < ns_cta;
       if (!smp && !synced) {
         TRACE(3);
-        seed_publish(tracker_key(tr, p.seed_h));
+        seed_publish(seed_key());
         synced = true;
         // wait (bounded) for this query's seeded threshold: the TMA producer and the MMA run
         // on meanwhile (four accumulators of slack), and the first store tiles are then
         // filtered by the seed instead of inserting from an empty list
         if (active) {
-          unsigned long long t0, t1;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          const long long t0 = clock64();
           for (;;) {
             unsigned dn;
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(dn) : "l"(p.seed_done + slab * M + m) : "memory");
             if (dn == s_epoch) break;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-            if ((long long)(t1 - t0) > p.seed_wait_ns) break;
+            if (clock64() - t0 > 2 * p.seed_wait_ns) break;
             __nanosleep(256);
           }
         }
+        __syncwarp();  // reconverge before the warp-collective barrier / tcgen05.ld below
         TRACE(10);
         gt_next = tk.peek_shared();
       }
@@ -537,6 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (smp) {
         // ---- a sample tile: only the tracker (the store pass scans these rows again)
+        if (i < 2) TRACE(16);
 #pragma unroll 1
         for (int c = 0; c < kTileN / 32; ++c) {
           uint32_t v[32];
@@ -547,28 +581,53 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
           }
+          // no per-lane early exit here: the next chunk's tcgen05.ld is warp-collective
           const float* xc = xs + c * 32;
-          unsigned mask = 0;
+          const int left = active ? ti.nvalid - c * 32 : 0;
+          {
+            // the chunk's best column by an argmax tree on (dot, den) pairs compared by
+            // cross-multiplication (den > 0): no division, five levels of independent compares
+            float bd[32], bn[32];
+            int bi[32];
 #pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
-            const float4 x4 = lds128f(xc + 4 * j4);
-            const float xx[4] = {x4.x, x4.y, x4.z, x4.w};
+            for (int j4 = 0; j4 < 8; ++j4) {
+              const float4 x4 = lds128f(xc + 4 * j4);
+              const float xx[4] = {x4.x, x4.y, x4.z, x4.w};
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int j = 4 * j4 + u;
-              mask |= (tr.may_pass(__uint_as_float(v[j]), __fmaf_rn(qn, xx[u], p.sigma)) ? 1u : 0u) << j;
+              for (int u = 0; u < 4; ++u) {
+                const int j = 4 * j4 + u;
+                bd[j] = j < left ? __uint_as_float(v[j]) : -__int_as_float(0x7f800000);
+                bn[j] = __fmaf_rn(qn, xx[u], p.sigma);
+                bi[j] = j;
+              }
+            }
+#pragma unroll
+            for (int w = 16; w > 0; w >>= 1) {
+#pragma unroll
+              for (int j = 0; j < w; ++j) {
+                const bool up = bd[j + w] * bn[j] > bd[j] * bn[j + w];
+                bd[j] = up ? bd[j + w] : bd[j];
+                bn[j] = up ? bn[j + w] : bn[j];
+                bi[j] = up ? bi[j + w] : bi[j];
+              }
+            }
+            // ... kept in a sorted list of the kHS best chunk maxima (h of them are published:
+            // each is a real key of this state, so its h-th is still a valid bound)
+            float nd = bd[0], nn = bn[0];
+            uint32_t ng = (uint32_t)(ti.gbase + (int64_t)(c * 32 + bi[0]) * ti.gstride);
+            if (left > 0 && nd * tr_den[kHS - 1] > tr_dot[kHS - 1] * nn) {
+#pragma unroll
+              for (int q = 0; q < kHS; ++q) {
+                const bool up = nd * tr_den[q] > tr_dot[q] * nn;
+                const float d0 = tr_dot[q], n0 = tr_den[q];
+                const uint32_t g0 = tr_gid[q];
+                tr_dot[q] = up ? nd : d0; tr_den[q] = up ? nn : n0; tr_gid[q] = up ? ng : g0;
+                nd = up ? d0 : nd; nn = up ? n0 : nn; ng = up ? g0 : ng;
+              }
             }
           }
-          const int left = ti.nvalid - c * 32;
-          if (left < 32) mask &= left > 0 ? ((1u << left) - 1u) : 0u;
-          while (mask) {
-            const int j = __ffs(mask) - 1;
-            mask &= mask - 1;
-            const float den = __fmaf_rn(qn, xc[j], p.sigma);
-            const float vj = __uint_as_float(sel32(v, j));
-            if (vj >= tr.tlim * den) tr.insert(make_key(__fdiv_rn(vj, den), ti.gbase + (c * 32 + j) * ti.gstride));
-          }
         }
+        if (i < 2) TRACE(17);
         continue;
       }
 #pragma unroll 1
@@ -664,7 +723,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if constexpr (KR > 0) tk.publish();
     }
-    if (!synced) seed_publish(tracker_key(tr, p.seed_h));  // this parity had no store tile
+    if (!synced) seed_publish(seed_key());  // this parity had no store tile
     TRACE(8);
     if (KR > 0 && p.merge_in_cta) {
       // Merge the two parity states of each query inside the CTA (one list per CTA per
@@ -695,7 +754,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
   TRACE(9);
-  if (p.trace && threadIdx.x == 0) p.trace[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + 12] = clock64();
+  if (p.trace && threadIdx.x == 0) p.trace[(blockIdx.y * gridDim.x + blockIdx.x) * kTraceSlots + 12] = clock64();
   if (C > 1) {  // no CTA leaves while a peer may still arrive on its barriers
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
@@ -816,12 +875,12 @@ static int g_max_stages = 0;
 // slab_rows: query rows stored per K-block (M for a full slab).
 static size_t tc_smem(int M, int slab_rows, int D, int nst, int buf_bytes) {
   return (size_t)dyn_smem_pad() + (size_t)(D / kBlockK) * slab_rows * 128 + (size_t)nst * kStageBytes +
-         (3 * (size_t)nst + 2 * kAcc + 4) * 8 + 4 * kTileN * 4 + (size_t)M * 8 + (size_t)buf_bytes;
+         (3 * (size_t)nst + 2 * kAcc + 4) * 8 + 4 * kTileN * 4 + (size_t)M * 12 + (size_t)buf_bytes;
 }
 
 static int tc_stages(int M, int D, int buf_bytes, int slab_rows = 0) {
   const long avail = (long)kMaxSmem - (long)tc_smem(M, slab_rows > 0 ? slab_rows : M, D, 0, buf_bytes);
-  const long n = avail / (kStageBytes + 16);
+  const long n = avail / (kStageBytes + 24);  // a stage: its 16 KB + three mbarriers (full, empty, cempty)
   const int cap = g_max_stages > 0 ? g_max_stages : kMaxStages;
   return (int)(n > cap ? cap : n);
 }
@@ -930,7 +989,7 @@ static cudaError_t launch_tc_m(const TcPlan* t, const TcArgs& a, dim3 g, cudaStr
 remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc, int k, float sigma,
                        const float* xnorm, int64_t n_rows, int64_t gid_offset, int64_t gid_stride,
                        uint64_t* cand_buf, unsigned long long* gthr, uint64_t* lists, cudaStream_t st,
-                       int* launches, int* lists_per_query, const TcSeedUse* seed) {
+                       int* launches, int* lists_per_query, const TcSeedUse* seed, bool norms_in_kernel) {
   if (!t->ok) return REMOE_ERR_UNSUPPORTED;
   // M = 128 when the 128-query slab still leaves >= 4 stages, else 64.  Candidate
   // buffers go to shared memory when that still leaves >= 4 stages.
@@ -976,9 +1035,9 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
     a.cluster = kn.no_multicast ? 1 : 8;  // reduced to what fits in launch_tc_t
     a.epi_sleep = kn.epi_sleep;
     a.xt = t->xt;
-    a.kb_order = kn.kb_order;
     a.slab_rows = SR;
     a.dbg = kn.dbg;
+    a.norms_in_kernel = norms_in_kernel ? 1 : 0;
     if (seed && t->xt && 2 * ctas_per_slab <= 320 && seed->store->keys && seed->store->tags && seed->store->done) {
       const TcSeed& sd = *seed->store;
       a.seed_xt = sd.xt;
@@ -1006,38 +1065,28 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
     }
     const int n_cta = ctas_per_slab * ns;
     if (kn.trace) {  // debug: per-CTA globaltimer stamps of the launch phases (this plan's buffer)
-      if (!t->trace_buf && cudaMalloc(&t->trace_buf, (size_t)t->grid * 16 * 8) != cudaSuccess) return REMOE_ERR_OOM;
-      cudaMemsetAsync(t->trace_buf, 0, (size_t)n_cta * 16 * 8, st);
+      if (!t->trace_buf && cudaMalloc(&t->trace_buf, (size_t)t->grid * kTraceSlots * 8) != cudaSuccess) return REMOE_ERR_OOM;
+      cudaMemsetAsync(t->trace_buf, 0, (size_t)n_cta * kTraceSlots * 8, st);
       a.trace = t->trace_buf;
     }
     const dim3 g((unsigned)ctas_per_slab, (unsigned)ns);
     cudaError_t e = (M == 128) ? launch_tc_m<128>(t, a, g, st) : launch_tc_m<64>(t, a, g, st);
     if (e != cudaSuccess) return REMOE_ERR_CUDA;
     if (a.trace) {
-      std::vector<unsigned long long> h((size_t)n_cta * 16);
+      std::vector<unsigned long long> h((size_t)n_cta * kTraceSlots);
       cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
       unsigned long long t0 = ~0ull;
-      for (int c = 0; c < n_cta; ++c) if (h[c * 16] && h[c * 16] < t0) t0 = h[c * 16];
+      for (int c = 0; c < n_cta; ++c) if (h[c * kTraceSlots] && h[c * kTraceSlots] < t0) t0 = h[c * kTraceSlots];
       fprintf(stderr, "[remoe] tc trace (us from first CTA start; CTA 0 | max over CTAs): nq %d k %d tiles %lld\n",
               a.nq, k, (long long)((n_rows + kTileN - 1) / kTileN));
-      const char* names[11] = {"start", "setup", "slab", "seed sync in", "mma first full", "mma tile0 commit",
-                               "epi pdl_wait", "epi first tfull", "epi loop done", "end", "seed sync out"};
-      {  // effective SM clock over the CTA's lifetime: clock64 ticks / globaltimer ns
-        double f = 0; int nf = 0;
-        for (int c = 0; c < n_cta; ++c)
-          if (h[c * 16 + 9] > h[c * 16] && h[c * 16 + 12] > h[c * 16 + 11]) {
-            f += (double)(h[c * 16 + 12] - h[c * 16 + 11]) / (double)(h[c * 16 + 9] - h[c * 16]); ++nf;
-          }
-        fprintf(stderr, "  effective SM clock %.0f MHz (mean over %d CTAs)\n", nf ? 1e3 * f / nf : 0.0, nf);
-        double lp = 0, wf = 0, wt = 0;
-        for (int c = 0; c < n_cta; ++c) { lp += h[c * 16 + 13]; wf += h[c * 16 + 14]; wt += h[c * 16 + 15]; }
-        fprintf(stderr, "  MMA issuer cycles (mean per CTA): loop %.0f, waiting full %.0f (%.0f%%), waiting tempty %.0f (%.0f%%)\n",
-                lp / n_cta, wf / n_cta, 100 * wf / (lp + 1), wt / n_cta, 100 * wt / (lp + 1));
-      }
-      for (int i = 0; i < 11; ++i) {
+      const char* names[22] = {"start", "setup", "slab", "seed publish", "", "mma tile0 commit",
+                               "epi pdl_wait", "epi first tfull", "epi loop done", "end", "seed ready", "", "", "", "",
+                               "", "sample tile start", "sample tile end", "", "", "", ""};
+      for (int i = 0; i < 20; ++i) {
+        if (!names[i][0]) continue;
         unsigned long long mx = 0;
-        for (int c = 0; c < n_cta; ++c) if (h[c * 16 + i] > mx) mx = h[c * 16 + i];
+        for (int c = 0; c < n_cta; ++c) if (h[c * kTraceSlots + i] > mx) mx = h[c * kTraceSlots + i];
         fprintf(stderr, "  %-18s %9.2f | %9.2f\n", names[i], h[i] ? (h[i] - t0) / 1e3 : -1.0,
                 mx ? (mx - t0) / 1e3 : -1.0);
       }

@@ -60,10 +60,12 @@ struct FinalizeArgs {
 // set_thr[b] = (k-th best key) - 1 (threshold seeding from a row sample).  If fin is
 // non-null the same CTA then runs S6 + S7 for the query (fused finalize).  If bump is
 // non-null, *bump += 1 once (after the previous kernel completed): the seeding epoch.
+// reset_lower: lower[b] = 0 once read (the scan that follows starts from no threshold,
+// without a k_norms launch to zero it).
 cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride, int64_t lstride,
                          int k, uint64_t* out, cudaStream_t st, unsigned long long* set_thr = nullptr,
-                         const unsigned long long* lower = nullptr, const FinalizeArgs* fin = nullptr,
-                         int list_len = -1, unsigned* bump = nullptr);
+                         unsigned long long* lower = nullptr, const FinalizeArgs* fin = nullptr,
+                         int list_len = -1, unsigned* bump = nullptr, bool reset_lower = false);
 
 // S6 + S7 as a separate kernel (tree search path with world == 1).
 cudaError_t launch_finalize(const uint64_t* top, int B, int k, const FinalizeArgs& f, cudaStream_t st);

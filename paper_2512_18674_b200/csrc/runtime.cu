@@ -439,6 +439,7 @@ static remoe_status_t build_local(remoe_sps* h, const uint16_t* emb, const float
   const int mb = c.max_batch;
   ST_TRY(h->alloc((void**)&h->qnorm, (size_t)mb * 4));
   ST_TRY(h->alloc((void**)&h->gthr, (size_t)2 * mb * 8));  // [0, mb): main scan, [mb, 2mb): seed scan
+  CUDA_TRY(cudaMemsetAsync(h->gthr, 0, (size_t)2 * mb * 8, st));  // kept zero between chunks (k_merge resets)
   // ---- seeding sample: S rows j * stride, S a multiple
   // of 128, only for large shards.  The sample is read in place through a strided tensor
   // map; only its norms and global ids are copied.
@@ -623,8 +624,6 @@ remoe_status_t remoe_sps_build(const remoe_sps_config_t* cfg, const uint16_t* em
 static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k, const remoe::FinalizeArgs* fin,
                                  cudaStream_t st, int* launches) {
   const remoe_sps_config_t& c = h->cfg;
-  CUDA_TRY(remoe::launch_norms(q, bc, c.dim, h->qnorm, st, h->gthr, c.max_batch));
-  ++*launches;
   // ---- S2+S3
   int which = h->force_kernel;
   if (which == 0) {
@@ -636,6 +635,14 @@ static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k,
     return fail(REMOE_ERR_UNSUPPORTED, "CTA-pair tensor-core scan unavailable for this store");
   int grid = 0;  // sorted key lists per query produced by the scan
   remoe::TcSeedUse su;  // in-kernel seeding of the tensor-core scan (none: su.store == nullptr)
+  // S1: the resident-slab tensor-core scan computes the query norms in its prologue (and the
+  // previous chunk's merge left the shared thresholds at zero); the other paths launch
+  // k_norms, which also zeroes the thresholds
+  const bool fold_norms = which == 2 && (h->seed_inkernel || h->seed_mode == 0);
+  if (!fold_norms) {
+    CUDA_TRY(remoe::launch_norms(q, bc, c.dim, h->qnorm, st, h->gthr, c.max_batch));
+    ++*launches;
+  }
   CUDA_TRY(h->prof_mark(st, true));
   if (which == 1) {
     grid = h->grid_simt;
@@ -682,25 +689,25 @@ static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k,
     // prefix with stride ~1024 / k, each state's h-th best key, threshold = the r-th largest
     const remoe::TcSeed& ss = h->seed_store;
     if (which == 2 && seed && ss.n_seg > 0 && h->seed_inkernel) {
-      // every 64th row for k <= 32, every 32nd above (REMOE_SEED_SEGS overrides: 1..4
-      // segments = every 64th, 32nd, 16th, 8th row); the round-1 stride sweep at k = 128
-      // measured strides 8..32 within 3%, and a denser sample costs its bytes
-      int nseg = k <= 32 ? 1 : 2;
-      if (h->seed_segs > 0) nseg = h->seed_segs;
-      nseg = std::min(nseg, ss.n_seg);
-      const int hmax = k <= 32 ? 4 : 8;
-      int hh = 1;
+      // Each state publishes its best sample key (h = 1) and the threshold is the k-th largest
+      // of them (r = k): the sample needs >= 2k tiles, so the prefix grows with k (every 64th
+      // row, then 32nd, 16th, 8th; REMOE_SEED_SEGS overrides the segment count).  One key per
+      // 128-row block of a random-order sample: the k-th largest block maximum is about the
+      // k-th best row of the sample.
+      int nseg = 1;
+      while (nseg < ss.n_seg && ss.seg_t0[nseg] < 2 * k) ++nseg;
+      if (h->seed_segs > 0) nseg = std::min(h->seed_segs, ss.n_seg);
       const int ntl = ss.seg_t0[nseg];
-      while (hh < hmax && ((k + hh - 1) / hh > 32 || ntl < 2 * ((k + hh - 1) / hh))) hh *= 2;
-      const int rr = (k + hh - 1) / hh;
-      if (rr <= 32 && ntl >= 2 * rr) {
+      if (ntl >= 2 * k) {
         su.store = &ss;
         su.n_stiles = ntl;
-        su.h = hh;
-        su.r = rr;
+        su.h = 1;
+        su.r = k;
       }
     }
-    if ((which == 3 || !su.store) && sd && seed && 8 * k <= sd->rows && (int64_t)lists_min * ks >= k) {
+    // the separate seed-scan launch: the CTA-pair scan, and the tensor-core scan when in-kernel
+    // seeding is off (it needs k_norms' query norms and zeroed seed thresholds)
+    if ((which == 3 || (!su.store && !fold_norms)) && sd && seed && 8 * k <= sd->rows && (int64_t)lists_min * ks >= k) {
       // Scan the sample with a short register top-k (k_s keys per state, k_s = 1 for
       // k <= 32: a running max, no insertion work): the k-th best key of the union of the
       // per-CTA lists is a real key of the store, hence a lower bound of the final k-th
@@ -724,7 +731,8 @@ static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k,
         which == 3 ? remoe::tc_pair_scan(&h->tc, q, h->qnorm, bc, k, c.sigma, h->xnorm, c.n_local, c.global_offset,
                                          1, h->cand_buf, h->gthr, h->lists, st, &nl, &grid)
                    : remoe::tc_scan(&h->tc, q, h->qnorm, bc, k, c.sigma, h->xnorm, c.n_local, c.global_offset,
-                                    1, h->cand_buf, h->gthr, h->lists, st, &nl, &grid, su.store ? &su : nullptr);
+                                    1, h->cand_buf, h->gthr, h->lists, st, &nl, &grid, su.store ? &su : nullptr,
+                                    fold_norms);
     if (ts != REMOE_OK)
       return fail(ts, "tensor-core scan launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     *launches += nl;
@@ -736,12 +744,15 @@ static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k,
   // final k-th best key (every published value is some state's own k-th best or a
   // seeded strict bound), so the merge drops every key below it.
   const cudaError_t me = remoe::launch_merge(h->lists, bc, grid, (int64_t)grid * k, k, k, h->local_top, st, nullptr,
-                                             h->gthr, fin, -1, su.store ? h->seed_store.epoch : nullptr);
-  if (me != cudaSuccess && su.store) {
-    // the seeded scan published keys under the current epoch and nothing bumps it now:
-    // retire them so a later chunk cannot read them as its own
-    cudaMemsetAsync(h->seed_store.tags, 0, (size_t)c.max_batch * 2 * std::max(1, h->grid_tc) * sizeof(unsigned), st);
-    cudaMemsetAsync(h->seed_store.done, 0, (size_t)c.max_batch * sizeof(unsigned), st);
+                                             h->gthr, fin, -1, su.store ? h->seed_store.epoch : nullptr, true);
+  if (me != cudaSuccess) {
+    // nothing resets the thresholds / retires the published seed keys now: do it here, so a
+    // later chunk starts clean
+    cudaMemsetAsync(h->gthr, 0, (size_t)2 * c.max_batch * 8, st);
+    if (su.store) {
+      cudaMemsetAsync(h->seed_store.tags, 0, (size_t)c.max_batch * 2 * std::max(1, h->grid_tc) * sizeof(unsigned), st);
+      cudaMemsetAsync(h->seed_store.done, 0, (size_t)c.max_batch * sizeof(unsigned), st);
+    }
   }
   CUDA_TRY(me);
   ++*launches;

@@ -24,7 +24,6 @@ constexpr int kSeedStride = 64;
 // plan is created (remoe_sps_build), never on the launch path.
 struct TcKnobs {
   int promo = 3;             // REMOE_TC_PROMO: L2 promotion of TMA boxes (0 none, 1 64 B, 2 128 B, 3 256 B)
-  int kb_order = 0;          // REMOE_TC_KB_ORDER: K-block visiting order (tcgen05.cuh kb_at)
   bool full_slab = false;    // REMOE_TC_FULL_SLAB: always store M query rows per K-block
   bool global_bufs = false;  // REMOE_TC_GLOBAL_BUFS: LaneTopk buffers in global memory
   int stages = 0;            // REMOE_TC_STAGES: cap the stage ring (0: as many as fit)
@@ -38,7 +37,6 @@ struct TcKnobs {
     TcKnobs k;
     auto ival = [](const char* n, int d) { const char* e = getenv(n); return e ? atoi(e) : d; };
     k.promo = ival("REMOE_TC_PROMO", 3);
-    k.kb_order = ival("REMOE_TC_KB_ORDER", 0);
     k.full_slab = getenv("REMOE_TC_FULL_SLAB") != nullptr;
     k.global_bufs = getenv("REMOE_TC_GLOBAL_BUFS") != nullptr;
     k.stages = ival("REMOE_TC_STAGES", 0);
@@ -122,7 +120,8 @@ void tc_plan_destroy(TcPlan* t);
 remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc, int k, float sigma,
                        const float* xnorm, int64_t n_rows, int64_t gid_offset, int64_t gid_stride,
                        uint64_t* cand_buf, unsigned long long* gthr, uint64_t* lists, cudaStream_t st,
-                       int* launches, int* lists_per_query, const TcSeedUse* seed = nullptr);
+                       int* launches, int* lists_per_query, const TcSeedUse* seed = nullptr,
+                       bool norms_in_kernel = false);
 // Large batches: the CTA-pair (cta_group::2) GEMM-tiled scan (k_scan_pair.cu), same
 // output contract as tc_scan; 256 queries per pair.
 bool tc_pair_usable(const TcPlan* t);

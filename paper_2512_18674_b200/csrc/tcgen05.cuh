@@ -23,16 +23,6 @@ static __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap*
       : "memory");
 }
 
-// K-block visiting order (REMOE_TC_KB_ORDER; 0 = ascending, the default; 1 = even
-// K-blocks first).  Kept as an experiment knob: with 2-D boxes of 128 B per row the
-// ascending order lets each 256 B L2 promotion serve the next box, order 1 measured
-// ~18% more DRAM bytes.  The accumulation order is fixed per launch shape.
-static __device__ __forceinline__ int kb_at(int j, int nkb, int order) {
-  if (order == 0) return j;
-  const int ne = (nkb + 1) >> 1;
-  return j < ne ? 2 * j : 2 * (j - ne) + 1;
-}
-
 // 1-D bulk copy multicast into every CTA of cta_mask (same smem offset, each CTA's own
 // mbarrier at the same offset).
 static __device__ __forceinline__ void bulk_g2s_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar,

@@ -1,0 +1,7 @@
+#!/bin/bash
+out=gpurun_out/${1:-r02_samp5}; mkdir -p $out
+t() { local tag=$1; shift; env "$@" REMOE_TC_TRACE=1 timeout 120 python bench.py --config $CFG --batch $B --k $K --steps 1 --warmup 2 --no-cpu-baseline --no-scan-events > $out/trace_$tag.log 2>&1; }
+b() { local tag=$1; shift; env "$@" timeout 180 python bench.py --config $CFG --batch $B --k $K --steps 20 --warmup 5 --no-cpu-baseline > $out/bench_$tag.log 2>&1; }
+CFG=c2 B=16 K=10; t c2_16; b c2_16
+CFG=c3 B=64 K=16; t c3_64; b c3_64
+echo done
