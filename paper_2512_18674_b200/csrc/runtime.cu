@@ -203,10 +203,11 @@ struct remoe_sps {
     int B = -1, k = -1, kernel = -1;
     cudaGraphExec_t exec = nullptr;
     int launches = 0;
+    int scan_kernel = 0;  // the scan kernel the captured query runs (get_info after a replay)
     uint64_t used = 0;
     void reset() {
       if (exec) cudaGraphExecDestroy(exec);
-      exec = nullptr; q = ids = scores = pred = nullptr; B = k = kernel = -1; launches = 0; used = 0;
+      exec = nullptr; q = ids = scores = pred = nullptr; B = k = kernel = -1; launches = 0; scan_kernel = 0; used = 0;
     }
   } dg[kGraphCache];
   uint64_t dg_clock = 0;
@@ -969,12 +970,14 @@ static remoe_status_t query_device_graph(remoe_sps* h, const uint16_t* q, int B,
     }
     g->q = q; g->ids = ids; g->scores = scores; g->pred = pred;
     g->B = B; g->k = k; g->kernel = h->force_kernel; g->launches = launches;
+    g->scan_kernel = h->last_kernel;
   }
   g->used = ++h->dg_clock;
   CUDA_TRY(cudaGraphLaunch(g->exec, st));
   CUDA_TRY(cudaEventRecord(h->gev_done, st));
   CUDA_TRY(cudaStreamWaitEvent(caller, h->gev_done, 0));
   h->last_launches = g->launches;
+  h->last_kernel = g->scan_kernel;
   return REMOE_OK;
 }
 

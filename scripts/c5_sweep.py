@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--cooldown", type=float, default=1.0, help="seconds idle before each point")
     args = ap.parse_args()
     import torch
     import paper_2512_18674_b200 as remoe
@@ -53,7 +54,23 @@ def main():
     fl_w = torch.empty(2 * l2 // 4 + 1024, dtype=torch.int32, device=dev)
     fl_r = torch.zeros_like(fl_w)
 
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        nvh = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    except Exception:
+        nvh = None
+
+    def clocks():
+        if nvh is None:
+            return None
+        return {"sm_mhz": pynvml.nvmlDeviceGetClockInfo(nvh, pynvml.NVML_CLOCK_SM),
+                "reasons_mask": int(pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(nvh))}
+
     def run_point(B, k, kernel=0):
+        # cool-down: the tensor-bound points draw ~1 kW; a light point measured right after
+        # one ran up to 1.6x slower on the same box (power-cap transient, scripts/r02_repro_*)
+        time.sleep(args.cooldown)
         sps.set_kernel(kernel)
         ids = torch.empty((B, k), dtype=torch.int64, device=dev)
         sc = torch.empty((B, k), dtype=torch.float32, device=dev)
@@ -77,6 +94,7 @@ def main():
             return [s.elapsed_time(e) for s, e in ev], scan_ms, phases
 
         step, _, _ = one_pass(False)
+        clk = clocks()
         _, scan_ms, phases = one_pass(True)
         info = sps.info()
         chunks = max(1, phases // args.steps)
@@ -95,6 +113,7 @@ def main():
             "tensor_frac_step": flops / (med / 1e3) / 1e12 / tc,
             "intensity_flop_per_byte": flops / alg,
             "bound_by_roofline": "tensor" if flops / alg > tc * 1e12 / (hbm * 1e9) else "hbm",
+            "clocks_after_step_pass": clk,
         }
 
     t0 = time.time()
