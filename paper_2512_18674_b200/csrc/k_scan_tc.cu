@@ -24,6 +24,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <type_traits>
 #include <vector>
 
@@ -91,9 +92,8 @@ struct TcArgs {
   int64_t seed_off[4];
   int64_t seed_stride[4];
   int seed_h, seed_r;
-  uint64_t* seed_keys;       // [nq][2 * gridDim.x] published h-th keys (this launch's queries)
-  unsigned* seed_tags;       // [nq][2 * gridDim.x] epoch of each published key
-  unsigned* seed_done;       // [nq] epoch once the query's seeded threshold is set
+  uint64_t* seed_pub;        // [nq][2 * gridDim.x] published words: (h-th key >> 32) << 32 | epoch
+  uint64_t* seed_done;       // [nq] the query's seed word: (threshold score word) << 32 | epoch
   const unsigned* seed_epoch;  // the epoch of this query chunk (bumped by its merge kernel)
   long long seed_wait_ns;    // how long the seeding warp waits for all keys (then: the subset)
   int norms_in_kernel;       // S1 in the prologue (no k_norms launch; qnorm unused)
@@ -132,7 +132,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* cempty = bars + 2 * NST + 2 * kAcc;  // [NST] cluster-wide "slot free" (leader CTA)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NST + 2 * kAcc);
   volatile unsigned& s_epoch = *reinterpret_cast<unsigned*>(bars + 3 * NST + 2 * kAcc + 1);  // free slot before sXn
-  // [2 parities][2 buffers][128] tile x-norms, shared by the 4 warps of a parity
+  unsigned* s_epi_done = reinterpret_cast<unsigned*>(bars + 3 * NST + 2 * kAcc + 1) + 1;  // epilogue warps finished
+  // [kAcc][128] x-norms of the tile in accumulator acc: bulk-copied by the MMA warp with the
+  // tile (completing on tfull[acc]), so the epilogue never waits on a global load for them
   float* sXn = reinterpret_cast<float*>(bars + ((3 * NST + 2 * kAcc + 2 + 1) & ~1));
   // [M] per-query threshold shared by the two parity states of the CTA (register top-k)
   unsigned long long* pair_thr = reinterpret_cast<unsigned long long*>(sXn + 4 * kTileN);  // [M]
@@ -181,8 +183,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty[s], 1);
       mbar_init(&cempty[s], C);
     }
-    for (int s = 0; s < kAcc; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
+    // tfull: the x-norm copy's arrive.expect_tx + the accumulator commit
+    for (int s = 0; s < kAcc; ++s) { mbar_init(&tfull[s], 2); mbar_init(&tempty[s], 4); }
     for (int s = 0; s < M; ++s) pair_thr[s] = 0ull;
+    *s_epi_done = 0;
     if (seeding) s_epoch = *reinterpret_cast<const volatile unsigned*>(p.seed_epoch);
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap_x) : "memory");
@@ -308,6 +312,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tempty[acc], aph ^ 1u);
       if (p.trace) w_tempty += clock64() - c0;
       tc_fence_after();
+      if (lane == 0) {
+        // the tile's |x_j| into sXn[acc] (the epilogue released acc, so also its norms):
+        // 16-byte multiple of the valid rows (the norm arrays are padded for the rounding)
+        const bool smp = i < ns_cta;
+        const int64_t t = tile_of(i);
+        int nv;
+        const float* src;
+        if (smp) {
+          src = p.seed_xn + t * kTileN;
+          nv = kTileN;  // the sample's norms are padded to whole tiles
+        } else {
+          src = p.xnorm + t * kTileN;
+          nv = (int)min((int64_t)kTileN, p.n_rows - t * kTileN);
+        }
+        const uint32_t nb = (uint32_t)((nv * 4 + 15) & ~15);
+        mbar_arrive_expect_tx(&tfull[acc], nb);
+        bulk_g2s(sXn + acc * kTileN, src, nb, &tfull[acc]);
+      }
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kTileN);
       uint64_t da = da0;
       for (int kb = 0; kb < nkb; ++kb) {
@@ -352,38 +374,38 @@ __global__ void __launch_bounds__(kThreads, 1)
     // state) or 0 (no key).
     if (seeding) {
       pdl_wait();  // k_norms zeroes the shared thresholds first
+      TRACE(18);
       const int G2 = 2 * (int)gridDim.x;
       const unsigned ep = s_epoch;
       for (int mm = blockIdx.x; mm < nq; mm += gridDim.x) {
         const size_t base = (size_t)(slab * M + mm) * G2;
         const long long t0 = clock64();  // SM cycle counter: cheap (a %globaltimer read is not)
-        unsigned ready = 0;  // bit u: slot lane + 32 u has this epoch's key
+        unsigned ready = 0;  // bit u: slot lane + 32 u has this epoch's word
+        // the published keys' score words (key >> 32; 0 = no key).  Each word carries its
+        // epoch in the low half, so one relaxed 64-bit load (single-copy atomic) gives the
+        // key and its validity together: no fences, no second load.  Under a full-bandwidth
+        // store stream every L2 round trip costs microseconds (REMOE_TC_TRACE: key + fence +
+        // tag, then fence + key load, took ~9 us from the last publish to the threshold).
+        uint32_t hi[10];
+#pragma unroll
+        for (int u = 0; u < 10; ++u) hi[u] = 0u;
         for (;;) {
 #pragma unroll
           for (int u = 0; u < 10; ++u) {
             const int idx = lane + 32 * u;
             if (idx < G2 && !((ready >> u) & 1u)) {
-              // relaxed loads (independent, in flight together); one fence once all are
-              // seen (an acquire per load serialised ten L2 round trips per poll)
-              unsigned tg;
-              asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(tg) : "l"(p.seed_tags + base + idx) : "memory");
-              if (tg == ep) ready |= 1u << u;
+              unsigned long long w;
+              asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p.seed_pub + base + idx) : "memory");
+              if ((unsigned)w == ep) { ready |= 1u << u; hi[u] = (uint32_t)(w >> 32); }
             } else if (idx >= G2) {
               ready |= 1u << u;
             }
           }
           if (__all_sync(kFull, ready == 0x3FFu)) break;
           if (clock64() - t0 > 2 * p.seed_wait_ns) break;  // ~ns at <= 2 GHz
-          __nanosleep(128);
+          __nanosleep(64);
         }
-        __threadfence();  // acquire: the keys written before each seen tag
-        // the published keys' score words (key >> 32; 0 = no key)
-        uint32_t hi[10];
-#pragma unroll
-        for (int u = 0; u < 10; ++u) {
-          const int idx = lane + 32 * u;
-          hi[u] = (idx < G2 && ((ready >> u) & 1u)) ? (uint32_t)(__ldcg(p.seed_keys + base + idx) >> 32) : 0u;
-        }
+        if (mm == blockIdx.x) TRACE(19);
         // T = the r-th largest score word, by a 32-step radix select with warp-wide counts
         // (cost independent of r).  At least r published keys -- r distinct real keys of the
         // store -- are >= T << 32, so T << 32 - 1 is a strict lower bound of the k-th best
@@ -399,11 +421,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const uint64_t T = (uint64_t)pre << 32;
         if (lane == 0) {
+          // the epilogues take the threshold from the done word itself (no ordering against
+          // the shared threshold needed); the atomic only feeds later readers of gthr
+          const unsigned long long dw = ((unsigned long long)pre << 32) | ep;
+          asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p.seed_done + slab * M + mm), "l"(dw) : "memory");
           if (T != 0) atomicMax(gthr_sl + mm, (unsigned long long)(T - 1));
-          __threadfence();
-          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.seed_done + slab * M + mm), "r"(ep) : "memory");
         }
+        if (mm == blockIdx.x) TRACE(20);
       }
+    }
+    // Threshold broker (then, or from the start without seeding): copy every query's
+    // shared threshold gthr (raised by all states of all CTAs) into pair_thr about every
+    // 0.3 us, until the last epilogue warp is done; the epilogue reads only pair_thr.
+    pdl_wait();  // gthr zeroed by k_norms (no-op if already waited)
+    for (;;) {
+      for (int mm = lane; mm < nq; mm += 32) {
+        unsigned long long v;
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(gthr_sl + mm) : "memory");
+        if (v > *reinterpret_cast<volatile unsigned long long*>(pair_thr + mm)) atomicMax(pair_thr + mm, v);
+      }
+      if (*reinterpret_cast<volatile unsigned*>(s_epi_done) >= (unsigned)kEpiWarps) break;
+      __nanosleep(256);
     }
   } else {
     // ------------------------------------------------ epilogue warps 2..9
@@ -428,10 +466,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     TRACE(6);
     const float qn = active ? (p.norms_in_kernel ? sQn[m] : qnorm_sl[m]) : 0.f;
     const int slot = e * 32 + lane;
-    // the tile's |x_j|: one copy per parity, double buffered by iteration.  Written after
-    // the tile's accumulator wait: by then every warp of the parity has released the
-    // accumulator of tile i - 4, i.e. has finished with the buffer being overwritten.
-    float* xs_base = sXn + parity * 2 * kTileN;
     constexpr int kCap = 32 * (P > 0 ? P : 2);
     uint64_t* buf = p.smem_bufs ? sBuf + (size_t)slot * kCap
                                 : p.cand_buf + (cta_lin * kTcEpilogueThreads + slot) * kCap;
@@ -497,35 +531,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       return ti;
     };
-    // the tile's |x_j| (lane l loads rows 4l..4l+3), loaded one tile ahead
-    auto load_xn = [&](int64_t i) {
-      float4 x = make_float4(1.f, 1.f, 1.f, 1.f);
-      if (i >= n_it) return x;
-      const TileInfo ti = tile_info(i);
-      if (4 * lane + 3 < ti.nvalid) {
-        x = __ldg(reinterpret_cast<const float4*>(ti.xn) + lane);
-      } else {
-        if (4 * lane + 0 < ti.nvalid) x.x = __ldg(ti.xn + 4 * lane + 0);
-        if (4 * lane + 1 < ti.nvalid) x.y = __ldg(ti.xn + 4 * lane + 1);
-        if (4 * lane + 2 < ti.nvalid) x.z = __ldg(ti.xn + 4 * lane + 2);
-      }
-      return x;
-    };
     // Seeding hand-off, once per state, before its first store tile (or at the end when it
     // has none): publish the state's h-th best sample key with this launch's epoch.
     auto seed_publish = [&](uint64_t kh) {
       if (!active) return;
       const size_t slot = (size_t)(slab * M + m) * (2 * gridDim.x) + 2 * blockIdx.x + parity;
-      p.seed_keys[slot] = kh;
-      __threadfence();
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.seed_tags + slot), "r"(s_epoch) : "memory");
+      const unsigned long long w = (kh & 0xFFFFFFFF00000000ull) | s_epoch;  // one 64-bit store: key word + epoch
+      asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p.seed_pub + slot), "l"(w) : "memory");
     };
     bool synced = !seeding;
-    float4 xv_next = load_xn(parity);
     uint64_t pair_pub = 0;  // last value this state shared with its parity partner
-    uint64_t gt_next = tk.peek_shared();  // shared threshold, also read one tile ahead
+    // The epilogue issues no global load per tile: the x-norms arrive with the tile
+    // (sXn[acc]), the query's shared threshold through pair_thr (the broker warp copies
+    // gthr there).  Under a full-bandwidth stream an L2 round trip takes microseconds, and
+    // a per-tile load one tile ahead stalled the catch-up after the seed (~3 us per tile).
+    long long ep_wait = 0, ep_t0 = 0;  // REMOE_TC_TRACE: tfull wait cycles of the store tiles' loop
     for (int64_t i = parity; i < n_it; i += 2) {
       const bool smp = i < ns_cta;
+      if (p.trace && !smp && ep_t0 == 0) { ep_t0 = clock64(); ep_wait = 0; }
       if (!smp && !synced) {
         TRACE(3);
         seed_publish(seed_key());
@@ -533,34 +556,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         // wait (bounded) for this query's seeded threshold: the TMA producer and the MMA run
         // on meanwhile (four accumulators of slack), and the first store tiles are then
         // filtered by the seed instead of inserting from an empty list
+        uint64_t seeded = 0;
         if (active) {
           const long long t0 = clock64();
           for (;;) {
-            unsigned dn;
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(dn) : "l"(p.seed_done + slab * M + m) : "memory");
-            if (dn == s_epoch) break;
+            unsigned long long dw;
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(dw) : "l"(p.seed_done + slab * M + m) : "memory");
+            if ((unsigned)dw == s_epoch) {
+              if (dw >> 32) seeded = (dw & 0xFFFFFFFF00000000ull) - 1ull;  // strict lower bound
+              break;
+            }
             if (clock64() - t0 > 2 * p.seed_wait_ns) break;
-            __nanosleep(256);
+            __nanosleep(128);
           }
         }
+        if (seeded) atomicMax(pair_thr + m, (unsigned long long)seeded);
         __syncwarp();  // reconverge before the warp-collective barrier / tcgen05.ld below
         TRACE(10);
-        gt_next = tk.peek_shared();
       }
       const int acc = (int)(i % kAcc);
       const uint32_t aph = (uint32_t)(i / kAcc) & 1u;
       const TileInfo ti = tile_info(i);
-      const float4 xv = xv_next;
-      const uint64_t gt = gt_next;
-      xv_next = load_xn(i + 2);
-      gt_next = tk.peek_shared();
+      const long long tw0 = p.trace ? clock64() : 0;
       if (p.epi_sleep) mbar_wait_sleep(&tfull[acc], aph);
       else mbar_wait(&tfull[acc], aph);
-      float* xs = xs_base + ((i >> 1) & 1) * kTileN;
-      reinterpret_cast<float4*>(xs)[lane] = xv;  // the 4 warps write identical values
-      asm volatile("bar.sync %0, 128;" ::"r"(7 + parity) : "memory");  // the parity's 4 warps
+      if (p.trace) ep_wait += clock64() - tw0;
+      const float* xs = sXn + acc * kTileN;  // landed with the tile (tfull)
       if (i < 2) TRACE(7);
-      if (active && !smp) tk.raise(gt);
+      if (active && !smp) tk.raise(*reinterpret_cast<volatile unsigned long long*>(pair_thr + m));
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kTileN);
       if (p.dbg & 2) {  // debug (REMOE_TC_DBG=2): release the accumulator unread (wrong results)
@@ -576,11 +599,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t v[32];
           tmem_ld32(tbase + c * 32, v);
           tmem_wait_ld();
-          if (c == kTileN / 32 - 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
-          }
           // no per-lane early exit here: the next chunk's tcgen05.ld is warp-collective
           const float* xc = xs + c * 32;
           const int left = active ? ti.nvalid - c * 32 : 0;
@@ -627,6 +645,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
+        // release the accumulator -- and with it sXn[acc] -- only after the last chunk's
+        // norms were read (the MMA warp refills both for tile i + kAcc)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
         if (i < 2) TRACE(17);
         continue;
       }
@@ -635,11 +658,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t v[32];
         tmem_ld32(tbase + c * 32, v);
         tmem_wait_ld();
-        if (c == kTileN / 32 - 1) {  // every load of this accumulator has completed
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-        }
         if constexpr (KR > 0) {
           // the other parity state of this query lives in the same CTA: share its k-th best
           // through shared memory every chunk (exact: disjoint rows, own k-th best keys)
@@ -721,7 +739,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      // every tcgen05.ld of the tile completed and its last norms were read: release
+      // the accumulator and sXn[acc]
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
       if constexpr (KR > 0) tk.publish();
+    }
+    if (lane == 0) atomicAdd(s_epi_done, 1u);  // the broker warp stops after the last one
+    if (p.trace && lane == 0 && warp == 4) {  // quarter 0, parity 0: store-loop cycles, tfull waits
+      unsigned long long* tr = p.trace + (blockIdx.y * gridDim.x + blockIdx.x) * kTraceSlots;
+      tr[21] = (unsigned long long)(clock64() - ep_t0);
+      tr[22] = (unsigned long long)ep_wait;
     }
     if (!synced) seed_publish(seed_key());  // this parity had no store tile
     TRACE(8);
@@ -1038,7 +1067,7 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
     a.slab_rows = SR;
     a.dbg = kn.dbg;
     a.norms_in_kernel = norms_in_kernel ? 1 : 0;
-    if (seed && t->xt && 2 * ctas_per_slab <= 320 && seed->store->keys && seed->store->tags && seed->store->done) {
+    if (seed && t->xt && 2 * ctas_per_slab <= 320 && seed->store->pub && seed->store->done) {
       const TcSeed& sd = *seed->store;
       a.seed_xt = sd.xt;
       a.seed_xn = sd.xn;
@@ -1052,8 +1081,7 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
       }
       a.seed_h = seed->h;
       a.seed_r = seed->r;
-      a.seed_keys = sd.keys + (size_t)s0 * 2 * ctas_per_slab;
-      a.seed_tags = sd.tags + (size_t)s0 * 2 * ctas_per_slab;
+      a.seed_pub = sd.pub + (size_t)s0 * 2 * ctas_per_slab;
       a.seed_done = sd.done + s0;
       a.seed_epoch = sd.epoch;
       a.seed_wait_ns = sd.wait_ns;
@@ -1082,13 +1110,20 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
               a.nq, k, (long long)((n_rows + kTileN - 1) / kTileN));
       const char* names[22] = {"start", "setup", "slab", "seed publish", "", "mma tile0 commit",
                                "epi pdl_wait", "epi first tfull", "epi loop done", "end", "seed ready", "", "", "", "",
-                               "", "sample tile start", "sample tile end", "", "", "", ""};
-      for (int i = 0; i < 20; ++i) {
+                               "", "sample tile start", "sample tile end", "seedw pdl_wait", "seedw keys seen", "seedw done", ""};
+      for (int i = 0; i < 21; ++i) {
         if (!names[i][0]) continue;
         unsigned long long mx = 0;
         for (int c = 0; c < n_cta; ++c) if (h[c * kTraceSlots + i] > mx) mx = h[c * kTraceSlots + i];
         fprintf(stderr, "  %-18s %9.2f | %9.2f\n", names[i], h[i] ? (h[i] - t0) / 1e3 : -1.0,
                 mx ? (mx - t0) / 1e3 : -1.0);
+      }
+      const int cyc[5] = {13, 14, 15, 21, 22};
+      const char* cn[5] = {"mma loop cyc", "mma full wait", "mma tempty wait", "epi4 loop cyc", "epi4 tfull wait"};
+      for (int j = 0; j < 5; ++j) {
+        unsigned long long mx = 0, sum = 0;
+        for (int c = 0; c < n_cta; ++c) { mx = std::max(mx, h[c * kTraceSlots + cyc[j]]); sum += h[c * kTraceSlots + cyc[j]]; }
+        fprintf(stderr, "  %-18s %9llu | max %9llu | mean %9llu\n", cn[j], h[cyc[j]], mx, sum / n_cta);
       }
     }
     if (a.stats) {

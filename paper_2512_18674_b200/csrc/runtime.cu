@@ -401,7 +401,8 @@ static remoe_status_t build_local(remoe_sps* h, const uint16_t* emb, const float
   const size_t xbytes = (size_t)c.n_local * c.dim * 2;
   const size_t abytes = (size_t)c.n_local * h->LE * 4;
   ST_TRY(h->alloc((void**)&h->x, xbytes));
-  ST_TRY(h->alloc((void**)&h->xnorm, (size_t)c.n_local * 4));
+  // + 4 floats: the tensor-core scan bulk-copies a tile's norms in 16-byte units
+  ST_TRY(h->alloc((void**)&h->xnorm, (size_t)(c.n_local + 4) * 4));
   ST_TRY(h->alloc((void**)&h->act, abytes));
   const cudaMemcpyKind kind = c.inputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   CUDA_TRY(cudaMemcpyAsync(h->x, emb, xbytes, kind, st));
@@ -473,13 +474,12 @@ static remoe_status_t build_local(remoe_sps* h, const uint16_t* emb, const float
     remoe::TcSeed& sd = h->seed_store;
     if (sd.n_seg > 0) {
       const size_t slots = (size_t)mb * 2 * std::max(1, h->grid_tc);
-      ST_TRY(h->alloc((void**)&sd.keys, slots * 8));
-      ST_TRY(h->alloc((void**)&sd.tags, slots * sizeof(unsigned)));
+      ST_TRY(h->alloc((void**)&sd.pub, slots * 8));
       ST_TRY(h->alloc((void**)&sd.epoch, sizeof(unsigned)));
-      ST_TRY(h->alloc((void**)&sd.done, (size_t)mb * sizeof(unsigned)));
-      CUDA_TRY(cudaMemsetAsync(sd.tags, 0, slots * sizeof(unsigned), st));
-      CUDA_TRY(cudaMemsetAsync(sd.done, 0, (size_t)mb * sizeof(unsigned), st));
-      static const unsigned one = 1;  // epoch 0 would match the zeroed tags
+      ST_TRY(h->alloc((void**)&sd.done, (size_t)mb * 8));
+      CUDA_TRY(cudaMemsetAsync(sd.pub, 0, slots * 8, st));
+      CUDA_TRY(cudaMemsetAsync(sd.done, 0, (size_t)mb * 8, st));
+      static const unsigned one = 1;  // epoch 0 would match the zeroed words
       CUDA_TRY(cudaMemcpyAsync(sd.epoch, &one, sizeof one, cudaMemcpyHostToDevice, st));
       if (const char* e = getenv("REMOE_SEED_WAIT_US")) sd.wait_ns = 1000LL * std::max(0, atoi(e));
     }
@@ -751,8 +751,8 @@ static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k,
     // later chunk starts clean
     cudaMemsetAsync(h->gthr, 0, (size_t)2 * c.max_batch * 8, st);
     if (su.store) {
-      cudaMemsetAsync(h->seed_store.tags, 0, (size_t)c.max_batch * 2 * std::max(1, h->grid_tc) * sizeof(unsigned), st);
-      cudaMemsetAsync(h->seed_store.done, 0, (size_t)c.max_batch * sizeof(unsigned), st);
+      cudaMemsetAsync(h->seed_store.pub, 0, (size_t)c.max_batch * 2 * std::max(1, h->grid_tc) * 8, st);
+      cudaMemsetAsync(h->seed_store.done, 0, (size_t)c.max_batch * 8, st);
     }
   }
   CUDA_TRY(me);

@@ -83,9 +83,8 @@ struct TcSeed {
   int64_t seg_count[4] = {0, 0, 0, 0}, seg_off[4] = {0, 0, 0, 0}, seg_stride[4] = {0, 0, 0, 0};
   uint16_t* xt = nullptr;            // tiled sample [tiles][D/64][16 KB]
   float* xn = nullptr;               // its norms [tiles * 128] (padding rows: 1)
-  uint64_t* keys = nullptr;          // [max_batch][2 * grid] published keys
-  unsigned* tags = nullptr;          // [max_batch][2 * grid] their epochs (zeroed at build)
-  unsigned* done = nullptr;          // [max_batch] epoch once a query's seeded threshold is set
+  uint64_t* pub = nullptr;           // [max_batch][2 * grid] published (key >> 32) << 32 | epoch (zeroed at build)
+  uint64_t* done = nullptr;          // [max_batch] (threshold score word) << 32 | epoch, once seeded
   unsigned* epoch = nullptr;         // current epoch (starts at 1; bumped by each chunk's merge)
   long long wait_ns = 200000;        // REMOE_SEED_WAIT_US: the seeding warp's wait bound
 };
