@@ -73,6 +73,8 @@ struct TcArgs {
   int dbg;                 // REMOE_TC_DBG bits (experiments only; 1 = skip the MMA)
   int slab_rows;           // query rows stored per K-block (multiple of 8, <= M): a single
                            // slab of nq queries stores only ceil(nq/8) 8-row atoms
+  int qps;                 // queries per slab (M, or fewer when D is too large for an M-row
+                           // slab: D > 1536 keeps qps rows resident, the MMA still runs M)
   unsigned long long* trace;  // REMOE_TC_TRACE: [grid][16] globaltimer stamps
   unsigned long long* stats;  // REMOE_TC_STATS: [0] candidate columns, [1] inserts, [2] chunks with a candidate
   // ---- in-kernel threshold seeding (DESIGN.md §7 "threshold seeding"): each CTA first
@@ -160,12 +162,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   // the store tiles in the same order (tile = blockIdx.x + j * gridDim.x), so the slabs
   // read each tile at about the same time: HBM once, the other slabs hit L2.
   const int slab = blockIdx.y;
-  const int nq = min(M, p.nq - slab * M);
-  const uint16_t* qsl = p.q + (size_t)slab * M * D;
-  const float* qnorm_sl = p.qnorm + slab * M;
-  unsigned long long* gthr_sl = p.gthr + slab * M;
+  const int QS = p.qps;
+  const int nq = min(QS, p.nq - slab * QS);
+  const uint16_t* qsl = p.q + (size_t)slab * QS * D;
+  const float* qnorm_sl = p.qnorm + slab * QS;
+  unsigned long long* gthr_sl = p.gthr + slab * QS;
   const int lists_per_cta = p.merge_in_cta ? 1 : 2;
-  uint64_t* out_sl = p.out + (size_t)slab * M * gridDim.x * lists_per_cta * p.k;
+  uint64_t* out_sl = p.out + (size_t)slab * QS * gridDim.x * lists_per_cta * p.k;
   const size_t cta_lin = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
 
   // Cluster of C = p.cluster CTAs along y (consecutive slabs, same tile sequence): the
@@ -378,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int G2 = 2 * (int)gridDim.x;
       const unsigned ep = s_epoch;
       for (int mm = blockIdx.x; mm < nq; mm += gridDim.x) {
-        const size_t base = (size_t)(slab * M + mm) * G2;
+        const size_t base = (size_t)(slab * QS + mm) * G2;
         const long long t0 = clock64();  // SM cycle counter: cheap (a %globaltimer read is not)
         unsigned ready = 0;  // bit u: slot lane + 32 u has this epoch's word
         // the published keys' score words (key >> 32; 0 = no key).  Each word carries its
@@ -424,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // the epilogues take the threshold from the done word itself (no ordering against
           // the shared threshold needed); the atomic only feeds later readers of gthr
           const unsigned long long dw = ((unsigned long long)pre << 32) | ep;
-          asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p.seed_done + slab * M + mm), "l"(dw) : "memory");
+          asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p.seed_done + slab * QS + mm), "l"(dw) : "memory");
           if (T != 0) atomicMax(gthr_sl + mm, (unsigned long long)(T - 1));
         }
         if (mm == blockIdx.x) TRACE(20);
@@ -535,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // has none): publish the state's h-th best sample key with this launch's epoch.
     auto seed_publish = [&](uint64_t kh) {
       if (!active) return;
-      const size_t slot = (size_t)(slab * M + m) * (2 * gridDim.x) + 2 * blockIdx.x + parity;
+      const size_t slot = (size_t)(slab * QS + m) * (2 * gridDim.x) + 2 * blockIdx.x + parity;
       const unsigned long long w = (kh & 0xFFFFFFFF00000000ull) | s_epoch;  // one 64-bit store: key word + epoch
       asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p.seed_pub + slot), "l"(w) : "memory");
     };
@@ -561,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const long long t0 = clock64();
           for (;;) {
             unsigned long long dw;
-            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(dw) : "l"(p.seed_done + slab * M + m) : "memory");
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(dw) : "l"(p.seed_done + slab * QS + m) : "memory");
             if ((unsigned)dw == s_epoch) {
               if (dw >> 32) seeded = (dw & 0xFFFFFFFF00000000ull) - 1ull;  // strict lower bound
               break;
@@ -931,7 +934,15 @@ remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int 
   t->grid = 0;
   t->threads_per_cta_queries = kTcEpilogueThreads;
   if (dim % kBlockK != 0) { t->why = "D % 64 != 0"; return REMOE_OK; }
-  if (tc_stages(64, dim, 0) < 3) { t->why = "query slab does not fit shared memory (D > 1536)"; return REMOE_OK; }
+  // the resident slab holds max_qps query rows: 64 while that leaves >= 3 stages
+  // (D <= 1536), else the largest multiple of 8 that leaves >= 4 (D = 2048: 40, 4096: 16);
+  // larger batches take several slabs (or the CTA-pair scan)
+  t->max_qps = 0;
+  if (tc_stages(64, dim, 0, 64) >= 3) t->max_qps = 64;
+  else
+    for (int sr = 56; sr >= 8 && t->max_qps == 0; sr -= 8)
+      if (tc_stages(64, dim, 0, sr) >= 4) t->max_qps = sr;
+  if (t->max_qps == 0) { t->why = "even an 8-query slab does not fit shared memory"; return REMOE_OK; }
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q{};
   if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
@@ -1023,11 +1034,12 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
   // M = 128 when the 128-query slab still leaves >= 4 stages, else 64.  Candidate
   // buffers go to shared memory when that still leaves >= 4 stages.
   const int M = tc_stages(128, t->dim, 0) >= 4 ? 128 : 64;
+  const int QS = M == 128 ? 128 : t->max_qps;  // queries per slab
   const int buf_bytes = k <= 32 ? 0 : kTcEpilogueThreads * 32 * topk_P(k) * 8;
   // a single slab stores only the 8-row atoms its queries need (more stages for small B)
-  const int n_slabs_all = (bc + M - 1) / M;
+  const int n_slabs_all = (bc + QS - 1) / QS;
   const TcKnobs& kn = t->kn;
-  const int SR = (n_slabs_all == 1 && !kn.full_slab) ? ((bc + 7) / 8) * 8 : M;
+  const int SR = (n_slabs_all == 1 && !(kn.full_slab && QS == M)) ? ((bc + 7) / 8) * 8 : QS;
   const bool smem_bufs = k > 32 && tc_stages(M, t->dim, buf_bytes, SR) >= 4 && !kn.global_bufs;
   int nst = tc_stages(M, t->dim, smem_bufs ? buf_bytes : 0, SR);
   if (kn.stages >= 2 && kn.stages < nst) nst = kn.stages;
@@ -1037,13 +1049,13 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
   const int lists_per_cta = in_cta ? 1 : 2;
   // Query slabs of M: one launch covers up to grid slabs, each slab on grid / slabs CTAs
   // walking the store in the same tile order (L2 sharing of every tile across slabs).
-  const int n_slabs = (bc + M - 1) / M;
+  const int n_slabs = n_slabs_all;
   const int slabs_per_launch = n_slabs < t->grid ? n_slabs : t->grid;
   const int ctas_per_slab = t->grid / slabs_per_launch;
   *lists_per_query = ctas_per_slab * lists_per_cta;
   for (int sl0 = 0; sl0 < n_slabs; sl0 += slabs_per_launch) {
     const int ns = n_slabs - sl0 < slabs_per_launch ? n_slabs - sl0 : slabs_per_launch;
-    const int s0 = sl0 * M;
+    const int s0 = sl0 * QS;
     TcArgs a{};
     a.xnorm = xnorm;
     a.n_rows = n_rows;
@@ -1065,6 +1077,7 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
     a.epi_sleep = kn.epi_sleep;
     a.xt = t->xt;
     a.slab_rows = SR;
+    a.qps = QS;
     a.dbg = kn.dbg;
     a.norms_in_kernel = norms_in_kernel ? 1 : 0;
     if (seed && t->xt && 2 * ctas_per_slab <= 320 && seed->store->pub && seed->store->done) {

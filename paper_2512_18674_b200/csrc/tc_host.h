@@ -58,6 +58,7 @@ inline int seed_ks_for(int k) { return k <= 32 ? 1 : k <= 64 ? 2 : 4; }
 
 struct TcPlan {
   bool ok = false;            // tensor-core scan usable for this store
+  int max_qps = 64;           // queries per resident slab (64; fewer for D > 1536)
   const char* why = "not initialised";
   int grid = 0;               // persistent CTAs
   int threads_per_cta_queries = 0;  // per-CTA private top-k lanes

@@ -205,8 +205,9 @@ def test_degenerate_rows(kern):
 
 @pytest.mark.parametrize("B", [6, 9])
 def test_dims_and_table_shapes(B):
-    """D at the minimum (8), odd chunk counts (D=40, 776), D=4096 (streaming kernel only;
-    B = 9 takes its 8-query slab, which must be sized to fit shared memory), E=1 and E=256."""
+    """D at the minimum (8), odd chunk counts (D=40, 776: streaming kernel only), D=4096
+    (the streaming kernel's B = 9 takes its 8-query slab, which must be sized to fit shared
+    memory; the tensor-core scan a reduced slab), E=1 and E=256."""
     rng = np.random.default_rng(4)
     for D, L, E, n in [(8, 3, 1, 777), (40, 2, 256, 3000), (776, 27, 64, 5000), (4096, 4, 8, 2000)]:
         x = gen.f32_to_bf16_bits(rng.standard_normal((n, D)).astype(np.float32))
@@ -220,6 +221,37 @@ def test_dims_and_table_shapes(B):
             ids, sc, pred = run(s, q, 9)
             assert_parity(compare(q, x, a, 9, ids, sc, pred), f"D={D} E={E} B={B} {kern}")
         s.close()
+
+
+@pytest.mark.parametrize("D", [2048, 3072, 4096])
+def test_large_dim_reduced_slabs(D):
+    """D > 1536: the tensor-core scan keeps fewer query rows resident (40 at D = 2048, 16 at
+    4096) and takes several slabs above that; every kernel and the automatic
+    choice match the oracle, with a ragged tail, for batches around the slab size and k on
+    both sides of the register top-k (9, 40)."""
+    rng = np.random.default_rng(D)
+    n = 2000 + 77
+    x = gen.f32_to_bf16_bits(rng.standard_normal((n, D)).astype(np.float32))
+    a = rng.random((n, 4, 8)).astype(np.float32) + 1e-3
+    a /= a.sum(-1, keepdims=True)
+    q_all = gen.f32_to_bf16_bits(rng.standard_normal((100, D)).astype(np.float32))
+    q_all[5] = x[1234]  # an exact copy
+    s = make(x, a, max_k=64)
+    for B in (1, 9, 17, 41, 100):
+        q = q_all[:B]
+        for k in (9, 40):
+            s.set_kernel(0)
+            ids, sc, pred = run(s, q, k)
+            assert s.info().last_scan_kernel == (KERNELS["tc"] if B < 128 else KERNELS["pair"])
+            assert_parity(compare(q, x, a, k, ids, sc, pred), f"D={D} B={B} k={k} auto")
+            if B > 5:
+                assert ids[5, 0] == 1234
+            for kern in ("stream", "pair"):
+                if not kernel_available(s, kern):
+                    continue
+                ids, sc, pred = run(s, q, k)
+                assert_parity(compare(q, x, a, k, ids, sc, pred), f"D={D} B={B} k={k} {kern}")
+    s.close()
 
 
 def test_chunking_above_max_batch():
