@@ -68,6 +68,8 @@ struct PairArgs {
   uint64_t* out;           // lists[(q * lists_per_query + l) * k + i]
   int smem_bufs;
   int merge_in_cta;
+  int dbg;                 // REMOE_TC_DBG experiment bits (wrong results): 128 = load the query
+                           // box only for the first tile, 256 = the store box only for the first
 };
 }  // namespace
 
@@ -133,9 +135,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty[s], ph ^ 1u);  // the pair's MMA is done with this CTA's slot
         if (lane == 0) {
-          if (crank == 0) mbar_arrive_expect_tx(&full[s], 4 * kBox);  // both CTAs' A and B boxes
-          tma_load_2d_pair(sA + (size_t)s * kBox, &tmap_q, kb * kPBK, qrow0, full0 + 8u * (uint32_t)s);
-          tma_load_2d_pair(sB + (size_t)s * kBox, &tmap_x, kb * kPBK, xrow, full0 + 8u * (uint32_t)s);
+          const bool first = t == pair;
+          const bool la = first || !(p.dbg & 128), lb = first || !(p.dbg & 256);
+          if (crank == 0) mbar_arrive_expect_tx(&full[s], (la ? 2 : 0) * kBox + (lb ? 2 : 0) * kBox);  // both CTAs' boxes
+          if (la) tma_load_2d_pair(sA + (size_t)s * kBox, &tmap_q, kb * kPBK, qrow0, full0 + 8u * (uint32_t)s);
+          if (lb) tma_load_2d_pair(sB + (size_t)s * kBox, &tmap_x, kb * kPBK, xrow, full0 + 8u * (uint32_t)s);
         }
         __syncwarp();
         if (++s == NST) { s = 0; ph ^= 1u; }
@@ -488,6 +492,7 @@ remoe_status_t tc_pair_scan(TcPlan* t, const uint16_t* q, const float* qnorm, in
     a.out = lists + (size_t)s0 * (*lists_per_query) * k;
     a.smem_bufs = smem_bufs ? 1 : 0;
     a.merge_in_cta = in_cta ? 1 : 0;
+    a.dbg = t->kn.dbg;
     if (t->kn.verbose)
       fprintf(stderr, "[remoe] pair scan grid (%d,%d) stages %d lists/query %d\n", 2 * ppg, ng, nst,
               *lists_per_query);

@@ -157,7 +157,7 @@ struct remoe_sps {
   bool seed_inkernel = true;  // REMOE_SEED_INKERNEL=0: the separate seed-scan launch instead (A/B)
   int seed_segs = 0;          // REMOE_SEED_SEGS: sample segments used by the in-kernel seed (0: by k)
   uint64_t* seed_top = nullptr;
-  // -1 auto: seed when k > 32 or B >= seed_min_b; 1 always (REMOE_SEED=1); 0 never
+  // -1 auto: seed when k >= kSeedMinK or B >= seed_min_b; 1 always (REMOE_SEED=1); 0 never
   // (REMOE_SEED=0).  Without a seed every top-k state (a CTA's rows for one query) starts
   // from nothing and inserts ~k(1 + ln(R/k)) keys, most of them in the first tiles, when
   // all SMs insert at once and the store stream stalls (ncu PM sampling, profiles/).
@@ -669,7 +669,7 @@ static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k,
     int nl = 0;
     const int seed_min_b = c.n_local < remoe::kSeedSmallRows ? std::min(h->seed_min_b, remoe::kSeedMinBSmall)
                                                               : h->seed_min_b;
-    const bool seed = h->seed_mode == 1 || (h->seed_mode == -1 && (k > 32 || bc >= seed_min_b));
+    const bool seed = h->seed_mode == 1 || (h->seed_mode == -1 && (k >= remoe::kSeedMinK || bc >= seed_min_b));
     // Lists per query the seed scan will produce, at least: one per CTA of a query slab
     // (M >= 64 queries per slab) or per CTA pair of a 256-query group.
     // Sample density by k: the sample should hold ~k rows of a query's topic for its k-th

@@ -15,6 +15,9 @@ constexpr int kSimtMaxB = 0;  // the tensor-core scan is faster at every measure
 // Threshold seeding (runtime.cu): batches >= kSeedMinB (and every k > 32) first scan every
 // kSeedStride-th row with a k_s-key register top-k per state.
 constexpr int kSeedMinB = 32;
+// ... and every batch from k = kSeedMinK on: a state's warm-up inserts grow with k (the c5
+// sweep: k = 32 at B <= 16 ran at 0.71-0.82 of HBM unseeded, k = 64 seeded at 0.89-0.91)
+constexpr int kSeedMinK = 16;
 // Shards below kSeedSmallRows rows give each top-k state so few rows that the warm-up
 // inserts dominate: seed from kSeedMinBSmall queries on (measured on the c2 store).
 constexpr int64_t kSeedSmallRows = 512 * 1024;

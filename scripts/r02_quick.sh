@@ -12,5 +12,8 @@ try:
 except Exception as e: print('$spec failed', e)
 " >> $out/bench.txt
 done
-if [ -n "$TESTS" ]; then timeout 1200 python -m pytest tests -m gpu -q -x --timeout 600 $TESTS > $out/pytest.log 2>&1; echo "rc=$?" >> $out/pytest.log; fi
+# TESTS: test files (default tests/), KEXPR: a pytest -k expression
+if [ -n "$TESTS$KEXPR" ]; then
+  timeout 1200 python -m pytest ${TESTS:-tests} -m gpu -q -x --timeout 600 ${KEXPR:+-k "$KEXPR"} > $out/pytest.log 2>&1; echo "rc=$?" >> $out/pytest.log
+fi
 cat $out/trace_c2_16.txt $out/stats_c2_16.txt $out/bench.txt; tail -3 $out/pytest.log 2>/dev/null
