@@ -49,6 +49,9 @@ def parse():
                     help="debug: no per-scan CUDA events inside the timed steps (no roofline)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
+                    help="N > 1: the fused peer-memory exchange (DESIGN.md §8; falls back to NCCL "
+                         "if a rank cannot map its peers) or NCCL collectives")
     return ap.parse_args()
 
 
@@ -202,6 +205,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        os.environ["REMOE_FUSED_COMM"] = "1" if args.exchange == "fused" else "0"  # read at build
         dist.init_process_group("nccl", device_id=dev)
     cfg = gen.CONFIGS[args.config]
     B = args.batch or cfg.batch
@@ -344,6 +348,8 @@ def run_ours(args):
         "dtype": "bf16",
         "data": "synthetic (clustered bf16 embeddings, Zipf activation tables; gen/)",
         "config": {**workload(cfg, B, k), "parallelism": f"store row-sharded x{world}",
+                   **({"exchange": "fused peer-memory (CUDA IPC over NVLink)" if info.fused_exchange
+                       else "NCCL collectives"} if world > 1 else {}),
                    "l2": "flushed between steps (write 2xL2, then read 2xL2: cold and clean)" if flush else "not flushed",
                    "scan_kernel": kern},
         "roofline": ({"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",

@@ -255,6 +255,16 @@ REMOE_API remoe_status_t remoe_sps_tree_query(remoe_sps_t h, const uint16_t* q_b
  * cfg.rank, cfg.loopback_group = the group, nccl_unique_id = NULL); the exchanges are
  * device-to-device copies of exactly the bytes the NCCL collectives would move.
  * remoe_loopback_group_destroy returns REMOE_ERR_STATE while handles are still built.
+ *
+ * Fused exchange (environment REMOE_FUSED_COMM=1 at build, world <= 8):
+ * instead of collectives, the merge kernels store their outputs (local top-k keys,
+ * exchange 1; partial predictions, exchange 2 in the all-gather layout) straight into
+ * every rank's receive buffer and raise a per-rank flag; the consuming kernels wait on
+ * the flags (bounded: a trap after 120 s instead of a silent hang).  Between NCCL ranks
+ * the receive buffers are mapped through CUDA IPC (NVLink peer access on one node; the
+ * ranks agree at build, and all fall back to NCCL if any cannot map its peers); in a
+ * loopback group they are the members' own buffers.  remoe_sps_get_info reports which
+ * path a handle uses (fused_exchange).
  */
 REMOE_API remoe_status_t remoe_loopback_group_create(int32_t world, remoe_group_t* out);
 REMOE_API remoe_status_t remoe_loopback_group_destroy(remoe_group_t g);
@@ -286,6 +296,10 @@ typedef struct {
   int32_t last_launches;      /* kernels launched by the last query (all chunks) */
   int32_t scan_ctas;          /* grid of the scan kernel */
   int64_t device_bytes;       /* store + table + workspaces */
+  int32_t fused_exchange;     /* 1: world > 1 exchanges run as peer-memory stores fused into the
+                                 merge kernels (REMOE_FUSED_COMM=1 at build, every rank agreed);
+                                 0: NCCL collectives (or device copies in a loopback group) */
+  int32_t reserved_;
 } remoe_sps_info_t;
 REMOE_API remoe_status_t remoe_sps_get_info(remoe_sps_t h, remoe_sps_info_t* info);
 

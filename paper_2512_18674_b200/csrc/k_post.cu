@@ -75,12 +75,52 @@ __device__ __forceinline__ void block_sort_desc(uint64_t* a, int np2) {
   }
 }
 
+// ---------------------------------------------------------------- fused peer exchange
+// Thread 0 waits until flags[g] >= seq for every g (acquire, system scope: the data the
+// peers stored before raising their flag is visible), then the CTA proceeds.  Bounded by
+// kPeerWaitNs: a peer that never signals traps the kernel (an error, not a hung GPU).
+constexpr unsigned long long kPeerWaitNs = 120000000000ull;  // 120 s: ranks may be seconds apart at their first query
+__device__ __forceinline__ void peer_wait(const unsigned long long* flags, int G, unsigned long long seq) {
+  if (threadIdx.x == 0) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int g = 0; g < G; ++g) {
+      for (;;) {
+        unsigned long long v;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + g) : "memory");
+        if (v >= seq) break;
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > kPeerWaitNs) __trap();
+        __nanosleep(64);
+      }
+    }
+  }
+  __syncthreads();
+}
+// Whole CTA, after its peer stores: the last CTA of the grid raises this rank's flag in
+// every rank (release, system scope) and resets the counter for the next exchange.
+__device__ __forceinline__ void peer_signal(const PeerXchg& px) {
+  __threadfence_system();  // this CTA's peer stores before its arrival
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned done = atomicAdd(px.counter, 1u);
+    if (done == gridDim.x - 1) {
+      atomicExch(px.counter, 0u);
+      __threadfence_system();  // every CTA's stores (seen through the counter) before the flags
+      for (int g = 0; g < px.G; ++g)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(px.flag_dst[g]), "l"(px.seq) : "memory");
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, int n_lists,
                                                int64_t qstride, int64_t lstride, int list_len, int k,
                                                uint64_t* __restrict__ out,
                                                unsigned long long* __restrict__ set_thr,
                                                unsigned long long* __restrict__ lower,
-                                               FinalizeArgs fin, unsigned* __restrict__ bump, int reset_lower) {
+                                               FinalizeArgs fin, unsigned* __restrict__ bump, int reset_lower,
+                                               PeerXchg px) {
   __shared__ uint64_t cand[kSelCap];
   __shared__ uint64_t topk[256];
   __shared__ unsigned hist[256];
@@ -92,6 +132,9 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const int b = blockIdx.x;
   pdl_wait();  // the scan's lists and thresholds
+  // (key loads are ld.global.cg: L2-coherent, so keys a peer stored over NVLink during
+  // this kernel's lifetime -- fused exchange 1 -- are never read through a stale L1 line)
+  if (px.G > 0 && px.wait_flags) peer_wait(px.wait_flags, px.G, px.seq);  // fused exchange 1: every rank's keys
   // the scan is complete: a new seeding epoch for the next chunk (stale published keys of
   // this one can never be taken for the next one's)
   if (bump && b == 0 && t == 0) atomicAdd(bump, 1u);
@@ -108,7 +151,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
     if (it >= items) return 0ull;
     const int l = nch == 1 ? it : it / nch, c = it - l * nch;
     const int i = c * 32 + lane;
-    return i < list_len ? __ldg(base + (int64_t)l * lstride + i) : 0ull;
+    return i < list_len ? __ldcg(base + (int64_t)l * lstride + i) : 0ull;
   };
   // flat key f = l * list_len + i: the whole block reads 8 keys per thread per round
   // (one L2 round trip per 2048 keys, instead of one per 32 lists of a warp)
@@ -116,7 +159,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
   auto flat_key = [&](int64_t f) -> uint64_t {
     if (f >= n_keys) return 0ull;
     const int64_t l = f / list_len, i = f - l * list_len;
-    return __ldg(base + l * lstride + i);
+    return __ldcg(base + l * lstride + i);
   };
   auto append = [&](uint64_t key, uint64_t thr_lo) {  // whole warp; keys >= thr_lo to cand
     const unsigned m = __ballot_sync(kFull, key >= thr_lo);
@@ -146,7 +189,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
     for (int l = t; l < n_lists; l += blockDim.x) {
       const uint64_t* lp = base + (int64_t)l * lstride;
       int need = 1;
-      while (need < nch && __ldg(lp + 32 * need - 1) >= thr_lo) ++need;
+      while (need < nch && __ldcg(lp + 32 * need - 1) >= thr_lo) ++need;
       const int pos = atomicAdd(&n_items_s, need);
       for (int c = 0; c < need; ++c) items_s[pos + c] = ((uint32_t)l << 3) | (uint32_t)c;
     }
@@ -161,7 +204,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
         if (it < ni) {
           const uint32_t w = items_s[it];
           const int i = (int)(w & 7u) * 32 + lane;
-          if (i < list_len) kk[u] = __ldg(base + (int64_t)(w >> 3) * lstride + i);
+          if (i < list_len) kk[u] = __ldcg(base + (int64_t)(w >> 3) * lstride + i);
         }
       }
 #pragma unroll
@@ -172,7 +215,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
   // a much tighter bound than lb when the state lists are many (S4: 2 per CTA).
   if (n_lists >= k && n_lists <= kSelCap) {
     if (t == 0) prefix_s = 0ull;
-    for (int l = t; l < n_lists; l += blockDim.x) cand[l] = __ldg(base + (int64_t)l * lstride);
+    for (int l = t; l < n_lists; l += blockDim.x) cand[l] = __ldcg(base + (int64_t)l * lstride);
     __syncthreads();
     for (int i = t; i < n_lists; i += blockDim.x) {
       const uint64_t x = cand[i];
@@ -256,7 +299,12 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
     for (int i = t; i < nout; i += blockDim.x) topk[i] = cand[i];
   }
   __syncthreads();
-  for (int i = t; i < k; i += blockDim.x) out[(int64_t)b * k + i] = i < nout ? topk[i] : 0ull;
+  for (int i = t; i < k; i += blockDim.x) {
+    const uint64_t v = i < nout ? topk[i] : 0ull;
+    out[(int64_t)b * k + i] = v;
+    if (px.G > 0 && px.key_dst[0])  // fused exchange 1: straight into every rank's gathered slot
+      for (int g = 0; g < px.G; ++g) px.key_dst[g][(int64_t)b * k + i] = v;
+  }
   if (set_thr && t == 0) {
     // seeding: the k-th best key of a subset of rows, minus one (strict lower bound,
     // the subset's own rows stay admissible in the full scan)
@@ -269,21 +317,24 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
     __syncthreads();
     finalize_query(topk, k, b, fin, 0, fin.LE, true);
   }
+  if (px.G > 0 && px.flag_dst[0]) peer_signal(px);
 }
 
 cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride, int64_t lstride,
                          int k, uint64_t* out, cudaStream_t st, unsigned long long* set_thr,
                          unsigned long long* lower, const FinalizeArgs* fin, int list_len,
-                         unsigned* bump, bool reset_lower) {
+                         unsigned* bump, bool reset_lower, const PeerXchg* px) {
   if (B <= 0) return cudaSuccess;
   if (k > 256) return cudaErrorInvalidValue;
   if (list_len <= 0) list_len = k;
   FinalizeArgs f{};
   if (fin) f = *fin;
+  PeerXchg x{};
+  if (px) x = *px;
   cudaError_t e = set_smem_attrs_once((const void*)k_merge, 0);
   if (e != cudaSuccess) return e;
   return launch_pdl(k_merge, dim3(B), dim3(256), 0, st, in, n_lists, qstride, lstride, list_len, k, out, set_thr,
-                    lower, f, bump, reset_lower ? 1 : 0);
+                    lower, f, bump, reset_lower ? 1 : 0, x);
 }
 
 // ---------------------------------------------------------------- S6 + S7
@@ -320,6 +371,9 @@ __device__ __forceinline__ void finalize_query(const uint64_t* tb, int k, int b,
     }
   }
   if (f.pred == nullptr) return;
+  // destinations of the rows: pred, or (fused exchange 2) this rank's slot in every rank
+  const int no = f.n_pred_peer > 0 ? f.n_pred_peer : 1;
+  float* const* outs = f.n_pred_peer > 0 ? f.pred_peer : &f.pred;
   float z = e;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(kFull, z, off);
@@ -369,8 +423,10 @@ __device__ __forceinline__ void finalize_query(const uint64_t* tb, int k, int b,
           }
         }
       }
-      reinterpret_cast<float4*>(f.pred + (int64_t)b * f.LE)[ca] = acc_a;
-      if (vb) reinterpret_cast<float4*>(f.pred + (int64_t)b * f.LE)[cb] = acc_b;
+      for (int o = 0; o < no; ++o) {
+        reinterpret_cast<float4*>(outs[o] + (int64_t)b * f.LE)[ca] = acc_a;
+        if (vb) reinterpret_cast<float4*>(outs[o] + (int64_t)b * f.LE)[cb] = acc_b;
+      }
     }
     return;
   }
@@ -395,8 +451,10 @@ __device__ __forceinline__ void finalize_query(const uint64_t* tb, int k, int b,
         }
       }
     }
-    f.pred[(int64_t)b * f.LE + ja] = acc_a;
-    if (vb) f.pred[(int64_t)b * f.LE + jb] = acc_b;
+    for (int o = 0; o < no; ++o) {
+      outs[o][(int64_t)b * f.LE + ja] = acc_a;
+      if (vb) outs[o][(int64_t)b * f.LE + jb] = acc_b;
+    }
   }
 }
 
@@ -423,14 +481,16 @@ cudaError_t launch_finalize(const uint64_t* top, int B, int k, const FinalizeArg
 // out[i] = parts[0][i] + parts[1][i] + ... + parts[G-1][i], g ascending: every rank sums
 // the same gathered partials in the same order, so all ranks (and every batch position)
 // get identical bits (ncclAllReduce's ring order would not guarantee that).
-__global__ void k_psum(const float* __restrict__ parts, int G, int64_t stride, int64_t n, float* __restrict__ out) {
+__global__ void k_psum(const float* parts, int G, int64_t stride, int64_t n, float* __restrict__ out,
+                       const unsigned long long* __restrict__ wait_flags, unsigned long long seq) {
   pdl_wait();
+  if (wait_flags) peer_wait(wait_flags, G, seq);  // fused exchange 2: every rank's partial landed
   const int64_t step = (int64_t)gridDim.x * blockDim.x;
   if ((stride & 3) == 0 && (n & 3) == 0 && ((reinterpret_cast<uintptr_t>(parts) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n >> 2); i += step) {
-      float4 acc = __ldg(reinterpret_cast<const float4*>(parts) + i);
+      float4 acc = __ldcg(reinterpret_cast<const float4*>(parts) + i);
       for (int g = 1; g < G; ++g) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(parts + g * stride) + i);
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(parts + g * stride) + i);
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
       reinterpret_cast<float4*>(out)[i] = acc;
@@ -444,13 +504,14 @@ __global__ void k_psum(const float* __restrict__ parts, int G, int64_t stride, i
   }
 }
 
-cudaError_t launch_psum(const float* parts, int G, int64_t part_stride, int64_t n, float* out, cudaStream_t st) {
+cudaError_t launch_psum(const float* parts, int G, int64_t part_stride, int64_t n, float* out, cudaStream_t st,
+                        const unsigned long long* wait_flags, unsigned long long seq) {
   if (n <= 0) return cudaSuccess;
   const int64_t units = (n + 3) / 4;
   const unsigned grid = (unsigned)std::min<int64_t>((units + 255) / 256, 148 * 8);
   cudaError_t e = set_smem_attrs_once((const void*)k_psum, 0);
   if (e != cudaSuccess) return e;
-  return launch_pdl(k_psum, dim3(grid), dim3(256), 0, st, parts, G, part_stride, n, out);
+  return launch_pdl(k_psum, dim3(grid), dim3(256), 0, st, parts, G, part_stride, n, out, wait_flags, seq);
 }
 
 // ---------------------------------------------------------------- S8 plan

@@ -41,6 +41,7 @@ cudaError_t launch_norms(const uint16_t* x, int64_t n, int dim, float* out, cuda
 // partial prediction): only the winners this rank owns (offset <= gid < offset + n_local)
 // contribute, in r-ascending order; the others are skipped, so pred receives this rank's
 // partial P_g = sum over owned r of w_r S~_{id_r} (SURVEY §8(e) exchange 2).
+constexpr int kMaxPeers = 8;  // ranks of one NVLink/NVSwitch node
 struct FinalizeArgs {
   const float* act;
   int64_t offset;
@@ -51,6 +52,25 @@ struct FinalizeArgs {
   int64_t* ids;
   float* scores;
   float* pred;  // may be null: ids and scores only
+  // fused exchange 2 (PeerXchg): the rows go to pred_peer[g] + b * LE for every rank g
+  // instead of pred (pred stays non-null: "a prediction is wanted")
+  int n_pred_peer;
+  float* pred_peer[kMaxPeers];
+};
+
+// Fused peer-memory exchange (world > 1, REMOE_FUSED_COMM=1): the producing
+// kernel stores its outputs straight into every rank's receive buffer (peer pointers:
+// CUDA IPC over NVLink between processes, plain device pointers in a loopback group), and
+// its last CTA raises this rank's flag in every rank to `seq` (release, system scope).  The
+// consuming kernel first waits until every rank's flag is >= seq (acquire, bounded: a
+// trap instead of a silent hang).  Receive buffers are double-buffered by seq parity.
+struct PeerXchg {
+  int G;                                     // ranks; 0 = off
+  uint64_t* key_dst[kMaxPeers];              // S4 output: this rank's [B][k] slot in rank g
+  unsigned long long* flag_dst[kMaxPeers];   // this rank's flag in rank g (null: no signal)
+  unsigned* counter;                         // finished CTAs (the last one signals, resets it)
+  const unsigned long long* wait_flags;      // [G] flags to wait for before reading (or null)
+  unsigned long long seq;
 };
 
 // S4 / S5: per query, merge n_lists sorted key lists of length list_len (default k) into
@@ -65,14 +85,17 @@ struct FinalizeArgs {
 cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride, int64_t lstride,
                          int k, uint64_t* out, cudaStream_t st, unsigned long long* set_thr = nullptr,
                          unsigned long long* lower = nullptr, const FinalizeArgs* fin = nullptr,
-                         int list_len = -1, unsigned* bump = nullptr, bool reset_lower = false);
+                         int list_len = -1, unsigned* bump = nullptr, bool reset_lower = false,
+                         const PeerXchg* px = nullptr);
 
 // S6 + S7 as a separate kernel (tree search path with world == 1).
 cudaError_t launch_finalize(const uint64_t* top, int B, int k, const FinalizeArgs& f, cudaStream_t st);
 
 // Multi-GPU S7 combine: out[i] = sum_{g = 0..G-1} parts[g * part_stride + i] for i < n, g
 // ascending (a fixed order: every rank and every batch position gets the same bits).
-cudaError_t launch_psum(const float* parts, int G, int64_t part_stride, int64_t n, float* out, cudaStream_t st);
+// wait_flags (fused exchange 2): first wait until wait_flags[g] >= seq for every g < G.
+cudaError_t launch_psum(const float* parts, int G, int64_t part_stride, int64_t n, float* out, cudaStream_t st,
+                        const unsigned long long* wait_flags = nullptr, unsigned long long seq = 0);
 
 // S8: cold mask of the n_cold smallest entries per (query, layer).
 cudaError_t launch_plan(const float* pred, int B, int L, int E, int n_cold, uint8_t* mask,

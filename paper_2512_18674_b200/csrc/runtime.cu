@@ -136,6 +136,16 @@ struct remoe_sps {
   float* part_all = nullptr;       // gathered partials / all-to-all receive buffer (world > 1)
   size_t part_all_floats = 0;
   size_t xchg_ag_max = 32u << 20;  // exchange 2 by all-gather while world*B*LE*4 <= this
+  // fused peer-memory exchange (REMOE_FUSED_COMM=1): gathered / part_all are
+  // double-buffered by chunk parity; peers store into them directly and raise their flag
+  bool fused = false;
+  unsigned long long* xflag = nullptr;  // [2][world]: exchange-1 / exchange-2 flag of each rank
+  unsigned* xcount = nullptr;           // [2] finished-CTA counters of the two producing kernels
+  unsigned long long xseq = 0;          // chunks exchanged so far (identical on every rank)
+  uint64_t* p_gathered[remoe::kMaxPeers] = {};
+  float* p_part_all[remoe::kMaxPeers] = {};
+  unsigned long long* p_xflag[remoe::kMaxPeers] = {};
+  std::vector<void*> ipc_opened;        // peer allocations opened through CUDA IPC
   // host-path staging
   uint16_t* hq = nullptr;
   int64_t* hids = nullptr;
@@ -265,6 +275,8 @@ struct remoe_sps {
   }
   void release() {
     reset_graphs();
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
+    ipc_opened.clear();
     if (gev) { cudaEventDestroy(gev); gev = nullptr; }
     if (gev_done) { cudaEventDestroy(gev_done); gev_done = nullptr; }
     if (gst) { cudaStreamDestroy(gst); gst = nullptr; }
@@ -502,12 +514,20 @@ static remoe_status_t build_local(remoe_sps* h, const uint16_t* emb, const float
     // [mb][LE]; the gathered partials [G][mb][LE] when they fit xchg_ag_max, and always
     // the all-to-all receive slices [G][ceil(mb / G)][LE]
     const size_t G = (size_t)c.world, LE = (size_t)h->LE;
-    ST_TRY(h->alloc((void**)&h->gathered, G * mb * c.max_k * 8));
+    if (const char* e = getenv("REMOE_FUSED_COMM")) h->fused = atoi(e) != 0 && c.world <= remoe::kMaxPeers;
+    const size_t nbuf = h->fused ? 2 : 1;  // fused: double-buffered by chunk parity
+    ST_TRY(h->alloc((void**)&h->gathered, nbuf * G * mb * c.max_k * 8));
     ST_TRY(h->alloc((void**)&h->part, (size_t)mb * LE * 4));
     const size_t a2a = G * ((mb + G - 1) / G) * LE;
     const size_t ag = std::min(G * mb * LE, h->xchg_ag_max / 4);
     h->part_all_floats = std::max(a2a, ag);
-    ST_TRY(h->alloc((void**)&h->part_all, h->part_all_floats * 4));
+    ST_TRY(h->alloc((void**)&h->part_all, nbuf * h->part_all_floats * 4));
+    if (h->fused) {
+      ST_TRY(h->alloc((void**)&h->xflag, 2 * G * sizeof(unsigned long long)));
+      ST_TRY(h->alloc((void**)&h->xcount, 2 * sizeof(unsigned)));
+      CUDA_TRY(cudaMemsetAsync(h->xflag, 0, 2 * G * sizeof(unsigned long long), st));
+      CUDA_TRY(cudaMemsetAsync(h->xcount, 0, 2 * sizeof(unsigned), st));
+    }
   }
   ST_TRY(h->alloc((void**)&h->hq, (size_t)mb * c.dim * 2));
   ST_TRY(h->alloc((void**)&h->hids, (size_t)mb * c.max_k * 8));
@@ -530,17 +550,17 @@ static remoe_status_t agree_build(remoe_sps* h, remoe_status_t local, cudaStream
   const remoe_sps_config_t& c = h->cfg;
   const std::string local_err = g_err;
   int64_t* d = nullptr;
-  const size_t bytes = sizeof(int64_t) * 3 * (c.world + 1);
+  const size_t bytes = sizeof(int64_t) * 4 * (c.world + 1);
   if (cudaMalloc(&d, bytes) != cudaSuccess) {
     cudaGetLastError();
     return fail(REMOE_ERR_OOM, "agreement buffer");  // cannot take part: peers will see NCCL errors
   }
-  int64_t mine[3] = {c.global_offset, c.n_local, (int64_t)local};
-  std::vector<int64_t> all(3 * c.world);
+  int64_t mine[4] = {c.global_offset, c.n_local, (int64_t)local, h->fused ? 1 : 0};
+  std::vector<int64_t> all(4 * c.world);
   cudaError_t ce = cudaMemcpyAsync(d, mine, sizeof mine, cudaMemcpyHostToDevice, st);
-  ncclResult_t nr = ce == cudaSuccess ? ncclAllGather(d, d + 3, 3, ncclInt64, h->comm, st) : ncclSuccess;
+  ncclResult_t nr = ce == cudaSuccess ? ncclAllGather(d, d + 4, 4, ncclInt64, h->comm, st) : ncclSuccess;
   if (ce == cudaSuccess && nr == ncclSuccess)
-    ce = cudaMemcpyAsync(all.data(), d + 3, sizeof(int64_t) * 3 * c.world, cudaMemcpyDeviceToHost, st);
+    ce = cudaMemcpyAsync(all.data(), d + 4, sizeof(int64_t) * 4 * c.world, cudaMemcpyDeviceToHost, st);
   if (ce == cudaSuccess && nr == ncclSuccess) ce = cudaStreamSynchronize(st);
   cudaFree(d);
   if (local != REMOE_OK) {
@@ -550,17 +570,82 @@ static remoe_status_t agree_build(remoe_sps* h, remoe_status_t local, cudaStream
   if (nr != ncclSuccess) return fail(REMOE_ERR_NCCL, "build agreement: %s", ncclGetErrorString(nr));
   if (ce != cudaSuccess) return fail(REMOE_ERR_CUDA, "build agreement: %s", cudaGetErrorString(ce));
   for (int g = 0; g < c.world; ++g)
-    if (all[3 * g + 2] != REMOE_OK)
-      return fail((remoe_status_t)all[3 * g + 2], "rank %d failed its build (%s); every rank fails", g,
-                  remoe_status_string((remoe_status_t)all[3 * g + 2]));
+    if (all[4 * g + 2] != REMOE_OK)
+      return fail((remoe_status_t)all[4 * g + 2], "rank %d failed its build (%s); every rank fails", g,
+                  remoe_status_string((remoe_status_t)all[4 * g + 2]));
   int64_t expect = 0;
+  bool fused_all = true;
   for (int g = 0; g < c.world; ++g) {
-    if (all[3 * g] != expect)
+    if (all[4 * g] != expect)
       return fail(REMOE_ERR_INVALID_ARG, "shards do not tile [0, N): rank %d offset %lld, expected %lld",
-                  g, (long long)all[3 * g], (long long)expect);
-    expect += all[3 * g + 1];
+                  g, (long long)all[4 * g], (long long)expect);
+    expect += all[4 * g + 1];
+    fused_all = fused_all && all[4 * g + 3] != 0;
   }
   h->n_total = expect;
+  h->fused = fused_all;  // the fused exchange only if every rank asked for it
+  return REMOE_OK;
+}
+
+// Fused exchange between NCCL ranks: every rank exports CUDA IPC handles of
+// its receive buffers (gathered keys, partials, flags), the handles are all-gathered once,
+// and every rank opens its peers' (NVLink peer mappings on one node).  The ranks agree
+// (all-reduce MIN): if any rank cannot open every peer, none uses the fused path.
+static remoe_status_t setup_peers_nccl(remoe_sps* h, cudaStream_t st) {
+  const int G = h->cfg.world, r = h->cfg.rank;
+  struct Handles { cudaIpcMemHandle_t gathered, part_all, xflag; };
+  Handles mine{};
+  int ok = cudaIpcGetMemHandle(&mine.gathered, h->gathered) == cudaSuccess &&
+           cudaIpcGetMemHandle(&mine.part_all, h->part_all) == cudaSuccess &&
+           cudaIpcGetMemHandle(&mine.xflag, h->xflag) == cudaSuccess;
+  cudaGetLastError();
+  std::vector<Handles> all(G);
+  char* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, sizeof(Handles) * (G + 1) + sizeof(int)));
+  struct Free { char* p; ~Free() { cudaFree(p); } } fr{d};
+  int* dok = reinterpret_cast<int*>(d + sizeof(Handles) * (G + 1));
+  CUDA_TRY(cudaMemcpyAsync(d, &mine, sizeof mine, cudaMemcpyHostToDevice, st));
+  NCCL_TRY(ncclAllGather(d, d + sizeof(Handles), sizeof(Handles), ncclChar, h->comm, st));
+  CUDA_TRY(cudaMemcpyAsync(all.data(), d + sizeof(Handles), sizeof(Handles) * G, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (int g = 0; g < G; ++g) {
+    if (g == r) {
+      h->p_gathered[g] = h->gathered; h->p_part_all[g] = h->part_all; h->p_xflag[g] = h->xflag;
+      continue;
+    }
+    void* pg = nullptr; void* pp = nullptr; void* pf = nullptr;
+    if (ok && cudaIpcOpenMemHandle(&pg, all[g].gathered, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) h->ipc_opened.push_back(pg); else ok = 0;
+    if (ok && cudaIpcOpenMemHandle(&pp, all[g].part_all, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) h->ipc_opened.push_back(pp); else ok = 0;
+    if (ok && cudaIpcOpenMemHandle(&pf, all[g].xflag, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) h->ipc_opened.push_back(pf); else ok = 0;
+    cudaGetLastError();
+    h->p_gathered[g] = static_cast<uint64_t*>(pg);
+    h->p_part_all[g] = static_cast<float*>(pp);
+    h->p_xflag[g] = static_cast<unsigned long long*>(pf);
+  }
+  CUDA_TRY(cudaMemcpyAsync(dok, &ok, sizeof ok, cudaMemcpyHostToDevice, st));
+  NCCL_TRY(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, h->comm, st));
+  CUDA_TRY(cudaMemcpyAsync(&ok, dok, sizeof ok, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (!ok) {  // every rank falls back to the NCCL exchanges
+    for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
+    h->ipc_opened.clear();
+    h->fused = false;
+  }
+  return REMOE_OK;
+}
+
+// Fused exchange in a loopback group: the peers are the members' own device buffers.
+static remoe_status_t setup_peers_loopback(remoe_sps* const* hs, int G) {
+  bool all = true;
+  for (int g = 0; g < G; ++g) all = all && hs[g]->fused;
+  for (int m = 0; m < G; ++m) {
+    if (!all) { hs[m]->fused = false; continue; }
+    for (int g = 0; g < G; ++g) {
+      hs[m]->p_gathered[g] = hs[g]->gathered;
+      hs[m]->p_part_all[g] = hs[g]->part_all;
+      hs[m]->p_xflag[g] = hs[g]->xflag;
+    }
+  }
   return REMOE_OK;
 }
 
@@ -578,7 +663,8 @@ static remoe_status_t build_impl(remoe_sps* h, const uint16_t* emb, const float*
     ncclUniqueId id;
     std::memcpy(&id, c.nccl_unique_id, sizeof id);
     NCCL_TRY(ncclCommInitRank(&h->comm, c.world, id, c.rank));
-    return agree_build(h, build_local(h, emb, act, st), st);
+    ST_TRY(agree_build(h, build_local(h, emb, act, st), st));
+    return h->fused ? setup_peers_nccl(h, st) : REMOE_OK;
   }
   ST_TRY(build_local(h, emb, act, st));
   if (c.loopback_group) {
@@ -623,7 +709,7 @@ remoe_status_t remoe_sps_build(const remoe_sps_config_t* cfg, const uint16_t* em
 // the per-CTA lists.  With `fin` (world == 1) the merge CTA goes on to S5-S7 itself (ids,
 // scores, prediction); otherwise the local top-k keys land in h->local_top.
 static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k, const remoe::FinalizeArgs* fin,
-                                 cudaStream_t st, int* launches) {
+                                 cudaStream_t st, int* launches, const remoe::PeerXchg* px = nullptr) {
   const remoe_sps_config_t& c = h->cfg;
   // ---- S2+S3
   int which = h->force_kernel;
@@ -745,7 +831,7 @@ static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k,
   // final k-th best key (every published value is some state's own k-th best or a
   // seeded strict bound), so the merge drops every key below it.
   const cudaError_t me = remoe::launch_merge(h->lists, bc, grid, (int64_t)grid * k, k, k, h->local_top, st, nullptr,
-                                             h->gthr, fin, -1, su.store ? h->seed_store.epoch : nullptr, true);
+                                             h->gthr, fin, -1, su.store ? h->seed_store.epoch : nullptr, true, px);
   if (me != cudaSuccess) {
     // nothing resets the thresholds / retires the published seed keys now: do it here, so a
     // later chunk starts clean
@@ -879,19 +965,83 @@ static remoe_status_t exchange(remoe_sps* const* hs, int nh, Xchg x, int bc, int
   return REMOE_OK;
 }
 
+// Fused exchange (h->fused): this chunk's parity buffers and the PeerXchg of
+// each producing kernel.  Exchange 1: the S4 merge stores the local keys into every rank's
+// gathered[par][rank]; exchange 2 (all-gather layout): the S5 merge stores the partial rows
+// into every rank's part_all[par][rank]; each raises this rank's flag to xseq in every rank.
+static size_t gathered_par(const remoe_sps* h) {
+  return (size_t)(h->xseq & 1) * h->cfg.world * h->cfg.max_batch * h->cfg.max_k;
+}
+static size_t part_all_par(const remoe_sps* h) { return (size_t)(h->xseq & 1) * h->part_all_floats; }
+static remoe::PeerXchg fused_keys(const remoe_sps* h, int bc, int k) {
+  remoe::PeerXchg px{};
+  px.G = h->cfg.world;
+  for (int g = 0; g < px.G; ++g) {
+    px.key_dst[g] = h->p_gathered[g] + gathered_par(h) + (size_t)h->cfg.rank * bc * k;
+    px.flag_dst[g] = h->p_xflag[g] + h->cfg.rank;  // exchange-1 flags: [0, G)
+  }
+  px.counter = h->xcount;
+  px.seq = h->xseq;
+  return px;
+}
+static remoe_status_t stage_merge_fused(remoe_sps* h, int bc, int k, int64_t* ids, float* scores, bool want_pred,
+                                        bool ag, cudaStream_t st, int* launches) {
+  const remoe_sps_config_t& c = h->cfg;
+  remoe::FinalizeArgs f{h->act, c.global_offset, c.n_local, 2, h->LE, c.temperature, ids, scores,
+                        want_pred ? h->part : nullptr};
+  remoe::PeerXchg px{};
+  px.G = c.world;
+  px.wait_flags = h->xflag;  // every rank's exchange-1 flag
+  px.seq = h->xseq;
+  if (want_pred && ag) {
+    f.n_pred_peer = c.world;
+    for (int g = 0; g < c.world; ++g) {
+      f.pred_peer[g] = h->p_part_all[g] + part_all_par(h) + (size_t)c.rank * bc * h->LE;
+      px.flag_dst[g] = h->p_xflag[g] + c.world + c.rank;  // exchange-2 flags: [G, 2G)
+    }
+    px.counter = h->xcount + 1;
+  }
+  CUDA_TRY(remoe::launch_merge(h->gathered + gathered_par(h), bc, c.world, k, (int64_t)bc * k, k, h->global_top,
+                               st, nullptr, nullptr, &f, -1, nullptr, false, &px));
+  ++*launches;
+  return REMOE_OK;
+}
+
 // The multi-rank pipeline for the handles in hs[0..nh) (NCCL: this process's handle;
-// loopback: every rank of the group).  local(h) runs S1-S4 (or the tree search) into
-// h->local_top; then exchange 1, S5-S7 and exchange 2.  ids/scores/pred are per handle.
+// loopback: every rank of the group).  local(h, px) runs S1-S4 (or the tree search) into
+// h->local_top -- and, fused, into every rank's receive buffer (px); then exchange 1,
+// S5-S7 and exchange 2.  ids/scores/pred are per handle.  `fusable`: the local stage
+// honours px (the brute-force scan; the tree search does not).
 template <class LocalStage>
 static remoe_status_t query_ranks(remoe_sps* const* hs, int nh, int bc, int k, int64_t* const* ids,
                                   float* const* scores, float* const* pred, cudaStream_t st, int* launches,
-                                  LocalStage&& local) {
-  for (int i = 0; i < nh; ++i) ST_TRY(local(hs[i]));
-  ST_TRY(exchange(hs, nh, Xchg::Keys, bc, k, pred, st));
+                                  LocalStage&& local, bool fusable) {
   const bool want = pred != nullptr && pred[0] != nullptr;
-  for (int i = 0; i < nh; ++i) ST_TRY(stage_merge(hs[i], bc, k, ids[i], scores[i], want, st, launches));
-  if (!want) return REMOE_OK;
   const bool ag = xchg_allgather(hs[0], bc);
+  if (fusable && hs[0]->fused) {
+    for (int i = 0; i < nh; ++i) ++hs[i]->xseq;  // identical on every rank (same chunk sequence)
+    for (int i = 0; i < nh; ++i) {
+      const remoe::PeerXchg px = fused_keys(hs[i], bc, k);
+      ST_TRY(local(hs[i], &px));
+    }
+    for (int i = 0; i < nh; ++i) ST_TRY(stage_merge_fused(hs[i], bc, k, ids[i], scores[i], want, ag, st, launches));
+    if (!want) return REMOE_OK;
+    if (ag) {
+      for (int i = 0; i < nh; ++i) {
+        remoe_sps* h = hs[i];
+        CUDA_TRY(remoe::launch_psum(h->part_all + part_all_par(h), h->cfg.world, (int64_t)bc * h->LE,
+                                    (int64_t)bc * h->LE, pred[i], st, h->xflag + h->cfg.world, h->xseq));
+        ++*launches;
+      }
+      return REMOE_OK;
+    }
+    // all-to-all layout: the partials (h->part) go through the collectives below
+  } else {
+    for (int i = 0; i < nh; ++i) ST_TRY(local(hs[i], nullptr));
+    ST_TRY(exchange(hs, nh, Xchg::Keys, bc, k, pred, st));
+    for (int i = 0; i < nh; ++i) ST_TRY(stage_merge(hs[i], bc, k, ids[i], scores[i], want, st, launches));
+    if (!want) return REMOE_OK;
+  }
   ST_TRY(exchange(hs, nh, ag ? Xchg::PartsAllGather : Xchg::PartsAllToAll, bc, k, pred, st));
   for (int i = 0; i < nh; ++i) ST_TRY(stage_combine(hs[i], bc, pred[i], st, launches));
   if (!ag) ST_TRY(exchange(hs, nh, Xchg::SlicesBroadcast, bc, k, pred, st));
@@ -906,8 +1056,10 @@ static remoe_status_t query_chunk(remoe_sps* h, const uint16_t* q, int bc, int k
     return stage_scan(h, q, bc, k, &fin, st, launches);
   }
   remoe_sps* hs[1] = {h};
-  return query_ranks(hs, 1, bc, k, &ids, &scores, &pred, st, launches,
-                     [&](remoe_sps* hh) { return stage_scan(hh, q, bc, k, nullptr, st, launches); });
+  return query_ranks(
+      hs, 1, bc, k, &ids, &scores, &pred, st, launches,
+      [&](remoe_sps* hh, const remoe::PeerXchg* px) { return stage_scan(hh, q, bc, k, nullptr, st, launches, px); },
+      true);
 }
 
 static bool aligned(const void* p, size_t a) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) % a) == 0; }
@@ -1027,6 +1179,7 @@ remoe_status_t remoe_sps_query_group(remoe_group_t g, const uint16_t* q, int32_t
       return fail(REMOE_ERR_INVALID_ARG, "loopback ranks differ in dim, table shape or max_batch");
   }
   for (int r = 0; r < G; ++r) hs[r]->n_total = expect;
+  ST_TRY(setup_peers_loopback(hs, G));
   const bool want = pred != nullptr && pred[0] != nullptr;
   for (int r = 0; r < G; ++r) {
     ST_TRY(check_query(hs[r], q, B, k, ids[r], scores[r], want ? pred[r] : nullptr));
@@ -1048,8 +1201,10 @@ remoe_status_t remoe_sps_query_group(remoe_group_t g, const uint16_t* q, int32_t
       pc[r] = want ? pred[r] + (size_t)b0 * LE : nullptr;
     }
     const uint16_t* qc = q + (size_t)b0 * hs[0]->cfg.dim;
-    ST_TRY(query_ranks(hs, G, bc, k, ic.data(), sc.data(), want ? pc.data() : nullptr, st, &launches,
-                       [&](remoe_sps* hh) { return stage_scan(hh, qc, bc, k, nullptr, st, &launches); }));
+    ST_TRY(query_ranks(
+        hs, G, bc, k, ic.data(), sc.data(), want ? pc.data() : nullptr, st, &launches,
+        [&](remoe_sps* hh, const remoe::PeerXchg* px) { return stage_scan(hh, qc, bc, k, nullptr, st, &launches, px); },
+        true));
   }
   for (int r = 0; r < G; ++r) hs[r]->last_launches = launches;
   return REMOE_OK;
@@ -1238,7 +1393,7 @@ remoe_status_t remoe_sps_tree_query(remoe_sps_t h, const uint16_t* q, int32_t B,
     int64_t* ic = ids + (size_t)b0 * k;
     float* sc = scores + (size_t)b0 * k;
     float* pc = pred ? pred + (size_t)b0 * h->LE : nullptr;
-    auto local = [&](remoe_sps* hh) -> remoe_status_t {
+    auto local = [&](remoe_sps* hh, const remoe::PeerXchg*) -> remoe_status_t {
       CUDA_TRY(remoe::launch_norms(qc, bc, c.dim, hh->qnorm, st));
       CUDA_TRY(remoe::launch_tree_search(hh->tree, hh->x, hh->xnorm, c.dim, qc, hh->qnorm, bc, k, c.sigma,
                                          c.global_offset, hh->local_top, leaf ? leaf + b0 : nullptr,
@@ -1247,13 +1402,13 @@ remoe_status_t remoe_sps_tree_query(remoe_sps_t h, const uint16_t* q, int32_t B,
       return REMOE_OK;
     };
     if (c.world == 1) {
-      ST_TRY(local(h));
+      ST_TRY(local(h, nullptr));
       const remoe::FinalizeArgs f{h->act, c.global_offset, c.n_local, 0, h->LE, c.temperature, ic, sc, pc};
       CUDA_TRY(remoe::launch_finalize(h->local_top, bc, k, f, st));
       ++launches;
     } else {
       remoe_sps* hs[1] = {h};
-      ST_TRY(query_ranks(hs, 1, bc, k, &ic, &sc, &pc, st, &launches, local));
+      ST_TRY(query_ranks(hs, 1, bc, k, &ic, &sc, &pc, st, &launches, local, false));
     }
   }
   h->last_launches = launches;
@@ -1320,6 +1475,7 @@ remoe_status_t remoe_sps_get_info(remoe_sps_t h, remoe_sps_info_t* info) {
   info->last_launches = h->last_launches;
   info->scan_ctas = h->last_kernel >= 2 ? h->grid_tc : h->grid_simt;
   info->device_bytes = (int64_t)h->device_bytes;
+  info->fused_exchange = h->fused ? 1 : 0;
   return REMOE_OK;
 }
 

@@ -83,6 +83,8 @@ class SpsInfo(ctypes.Structure):
         ("last_launches", ctypes.c_int32),
         ("scan_ctas", ctypes.c_int32),
         ("device_bytes", ctypes.c_int64),
+        ("fused_exchange", ctypes.c_int32),
+        ("reserved_", ctypes.c_int32),
     ]
 
 

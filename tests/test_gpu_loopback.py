@@ -160,6 +160,43 @@ def test_loopback_pair_scan_and_no_pred():
     g.close()
 
 
+@pytest.mark.parametrize("G", [2, 3, 8])
+@pytest.mark.parametrize("xchg", ["allgather", "alltoall"])
+def test_loopback_fused_exchange(G, xchg, monkeypatch):
+    """REMOE_FUSED_COMM=1: the exchanges run as peer stores inside the merge kernels (the
+    S4 merge writes every rank's gathered[parity][rank], the S5 merge every rank's partial
+    slot, each last CTA raises its flag; the consumers wait on the flags) -- no copies.
+    Several chunks (max_batch 5 over B = 13) exercise both parity buffers and the flag
+    sequence; results equal the collective path bit for bit, the oracle, and world 1."""
+    if xchg == "alltoall":
+        monkeypatch.setenv("REMOE_XCHG_AG_MAX", "0")
+    c, x, a = store(50_001)
+    B, k = 13, 10
+    qb = gen.queries(c.store_seed, c.query_seed, 50_001, c.dim, B, mode=1)
+    g0 = group(x, a, G, max_k=16, max_batch=5)
+    ref = run_group(g0, qb, k)
+    assert g0.ranks[0].info().fused_exchange == 0
+    g0.close()
+    monkeypatch.setenv("REMOE_FUSED_COMM", "1")
+    g = group(x, a, G, max_k=16, max_batch=5)
+    for rep_i in range(3):  # repeated queries: the flag sequence keeps advancing
+        ids, sc, pred = run_group(g, qb, k)
+        assert g.ranks[0].info().fused_exchange == 1
+        check_ranks_identical(ids, sc, pred)
+        for r in range(G):
+            assert np.array_equal(ids[r], ref[0][r]) and np.array_equal(sc[r], ref[1][r])
+            assert np.array_equal(pred[r], ref[2][r]), "fused exchange == collective exchange, bit for bit"
+    ids2, sc2, _ = run_group(g, qb, k, want_pred=False)  # no prediction: exchange 1 only
+    assert np.array_equal(ids2[0], ids[0]) and np.array_equal(sc2[0], sc[0])
+    g.close()
+    rep = compare(qb, x, a, k, ids[0], sc[0], pred[0])
+    log_report(f"loopback fused G={G} {xchg} c2[50k] B={B} k={k}", rep)
+    assert rep.ok(), "\n".join(rep.failures[:20])
+    i1, s1, p1 = run_single(x, a, qb, k, max_k=16)
+    assert np.array_equal(ids[0], i1) and np.array_equal(sc[0], s1)
+    assert np.abs(pred[0] - p1).max() <= 1e-6
+
+
 def test_loopback_errors():
     c, x, a = store(1_000, "tiny")
     gid = remoe.remoe_loopback_group_create(2)
