@@ -49,6 +49,9 @@ def parse():
                     help="debug: no per-scan CUDA events inside the timed steps (no roofline)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--shard-of", type=int, default=1,
+                    help="N = 1 only: run the step on shard 0 of a G-way row split (the per-GPU "
+                         "work of G GPUs: S1-S7 on that shard, no exchange); a diagnostic line")
     ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
                     help="N > 1: the fused peer-memory exchange (DESIGN.md §8; falls back to NCCL "
                          "if a rank cannot map its peers) or NCCL collectives")
@@ -211,6 +214,10 @@ def run_ours(args):
     B = args.batch or cfg.batch
     k = args.k or cfg.k
     off, n_loc = gen.shard_range(cfg.n, world, rank)
+    if args.shard_of > 1:
+        if world > 1:
+            raise SystemExit("--shard-of is a one-GPU diagnostic")
+        off, n_loc = gen.shard_range(cfg.n, args.shard_of, 0)
 
     # ---- inputs: this rank's shard, generated on the host, copied into HBM at build
     x = gen.store_emb(cfg.store_seed, cfg.n, cfg.dim, off, n_loc)
@@ -218,7 +225,7 @@ def run_ours(args):
     if world > 1:
         from paper_2512_18674_b200.dist import build_sharded
         sps = build_sharded(x, a, cfg.n, device=local, max_batch=max(B, 1), max_k=max(k, 1))
-    else:
+    else:  # (with --shard-of: the shard alone, as a one-rank store of n_loc rows)
         sps = remoe.Sps(x, a, max_batch=max(B, 1), max_k=max(k, 1), device=local)
     if args.kernel != "auto":
         sps.set_kernel({"stream": remoe.KERNEL_STREAM, "tc": remoe.KERNEL_TC,
@@ -350,6 +357,9 @@ def run_ours(args):
         "config": {**workload(cfg, B, k), "parallelism": f"store row-sharded x{world}",
                    **({"exchange": "fused peer-memory (CUDA IPC over NVLink)" if info.fused_exchange
                        else "NCCL collectives"} if world > 1 else {}),
+                   **({"shard": f"diagnostic: shard 0 of {args.shard_of} ({n_loc:,} rows) alone on one GPU -- "
+                                f"the per-GPU scan work of {args.shard_of} GPUs, S1-S7 without the exchanges"}
+                      if args.shard_of > 1 else {}),
                    "l2": "flushed between steps (write 2xL2, then read 2xL2: cold and clean)" if flush else "not flushed",
                    "scan_kernel": kern},
         "roofline": ({"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
