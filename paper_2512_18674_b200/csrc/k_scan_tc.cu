@@ -103,9 +103,10 @@ struct TcArgs {
 }  // namespace
 
 // M = queries per pass (UMMA M, 64 or 128).  For M = 64 the accumulator rows live in
-// lanes 0-15 of each 32-lane TMEM quarter (row r -> lane 32*(r/16) + r%16).  Slab row
-// r = R*q + l (R = M/4 rows per quarter) holds query m = 4*l + q, so a batch smaller than
-// M spreads over all four epilogue quarters instead of filling the first one.
+// lanes 0-15 of each 32-lane TMEM quarter (row r -> lane 32*(r/16) + r%16); slab row m
+// holds query m, so query m is read by the epilogue warps of quarter m/16 (a batch of
+// <= 16 uses quarter 0's two warps: the epilogue is busy ~25% of the stream time at c3 --
+// REMOE_TC_TRACE -- and spreading the queries would need the full 64-row slab).
 #define TRACE(idx)                                                                              \
   do {                                                                                          \
     if (p.trace && (threadIdx.x & 31) == 0) {                                                   \
