@@ -434,6 +434,7 @@ __device__ __forceinline__ uint4 ldg_nc128(const void* p) {
 // keeps CAP - k >= 32 (room for a chunk after a compaction) for every k <= 256.  (CAP =
 // pow2ceil(4k) made the k > 64 scans spill: the P = 16 sort network needs more registers
 // than the epilogue has, and seeded thresholds leave the buffers nearly empty anyway.)
+// (k <= 256 = the API maximum gives P <= 16; the kernels instantiate P in {2, 4, 8, 16})
 __host__ __device__ constexpr int topk_P(int k) {
   return (2 * k <= 64) ? 2 : (2 * k <= 128) ? 4 : (2 * k <= 256) ? 8 : (2 * k <= 512) ? 16 : 32;
 }

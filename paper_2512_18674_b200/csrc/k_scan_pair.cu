@@ -426,7 +426,6 @@ static cudaError_t launch_pair(const TcPlan* t, const CUtensorMap& tq, const Pai
     case 4: return launch_pair_t<4, 0>(t, tq, a, g, st);
     case 8: return launch_pair_t<8, 0>(t, tq, a, g, st);
     case 16: return launch_pair_t<16, 0>(t, tq, a, g, st);
-    case 32: return launch_pair_t<32, 0>(t, tq, a, g, st);
   }
   return cudaErrorInvalidValue;
 }

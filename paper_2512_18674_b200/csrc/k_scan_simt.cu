@@ -209,7 +209,6 @@ static cudaError_t launch_bq(const SimtScanParams& p, int P, int grid, size_t sm
     case 4: return launch_t<BQ, 4>(p, grid, smem, st);
     case 8: return launch_t<BQ, 8>(p, grid, smem, st);
     case 16: return launch_t<BQ, 16>(p, grid, smem, st);
-    case 32: return launch_t<BQ, 32>(p, grid, smem, st);
   }
   return cudaErrorInvalidValue;
 }

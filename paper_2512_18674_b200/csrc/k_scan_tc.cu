@@ -1022,7 +1022,6 @@ static cudaError_t launch_tc_m(const TcPlan* t, const TcArgs& a, dim3 g, cudaStr
     case 4: return launch_tc_t<M, 4>(t, a, g, st);
     case 8: return launch_tc_t<M, 8>(t, a, g, st);
     case 16: return launch_tc_t<M, 16>(t, a, g, st);
-    case 32: return launch_tc_t<M, 32>(t, a, g, st);
   }
   return cudaErrorInvalidValue;
 }
