@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
                                                unsigned long long* __restrict__ set_thr,
                                                unsigned long long* __restrict__ lower,
                                                FinalizeArgs fin, unsigned* __restrict__ bump, int reset_lower,
-                                               PeerXchg px) {
+                                               PeerXchg px, unsigned* __restrict__ split_cnt) {
   __shared__ MergeScratch S;
   pdl_wait();  // the scan's lists and thresholds
   // (key loads are ld.global.cg: L2-coherent, so keys a peer stored over NVLink during
@@ -59,16 +59,23 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
   if (px.G > 0 && px.wait_flags) peer_wait(px.wait_flags, px.G, px.seq);  // fused exchange 1: every rank's keys
   // the scan is complete: a new seeding epoch for the next chunk (stale published keys of
   // this one can never be taken for the next one's)
-  if (bump && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(bump, 1u);
+  if (bump && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(bump, 1u);
+  // grid (B, n_split): split y redoes the (cheap) selection and reduces columns
+  // [y * chunk, (y + 1) * chunk) of the prediction -- the gather of the k activation rows,
+  // latency-bound in one CTA, spreads over n_split SMs; split 0 writes the keys, ids, scores
+  const int n_split = (int)gridDim.y;
+  const int64_t chunk = ((fin.LE + n_split - 1) / n_split + 3) & ~int64_t(3);
+  const int64_t j0 = (int64_t)blockIdx.y * chunk;
+  const int64_t j1 = j0 + chunk < fin.LE ? j0 + chunk : fin.LE;
   merge_query(in, blockIdx.x, n_lists, qstride, lstride, list_len, k, out, set_thr, lower, fin, reset_lower, &px,
-              threadIdx.x, [] { __syncthreads(); }, S);
+              threadIdx.x, [] { __syncthreads(); }, S, j0, j1, blockIdx.y == 0, split_cnt, n_split);
   if (px.G > 0 && px.flag_dst[0]) peer_signal(px);
 }
 
 cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride, int64_t lstride,
                          int k, uint64_t* out, cudaStream_t st, unsigned long long* set_thr,
                          unsigned long long* lower, const FinalizeArgs* fin, int list_len,
-                         unsigned* bump, bool reset_lower, const PeerXchg* px) {
+                         unsigned* bump, bool reset_lower, const PeerXchg* px, unsigned* split_cnt) {
   if (B <= 0) return cudaSuccess;
   if (k > 256) return cudaErrorInvalidValue;
   if (list_len <= 0) list_len = k;
@@ -78,8 +85,15 @@ cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride
   if (px) x = *px;
   cudaError_t e = set_smem_attrs_once((const void*)k_merge, 0);
   if (e != cudaSuccess) return e;
-  return launch_pdl(k_merge, dim3(B), dim3(256), 0, st, in, n_lists, qstride, lstride, list_len, k, out, set_thr,
-                    lower, f, bump, reset_lower ? 1 : 0, x);
+  // column splits of the finalize: ~2 CTAs per SM in total, >= 256 columns per split
+  int n_split = 1;
+  if (split_cnt && fin && f.pred && f.n_pred_peer == 0 && x.G == 0 && !set_thr) {
+    static int sms = 0;
+    if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) { cudaGetLastError(); sms = 148; }
+    n_split = (int)std::max<int64_t>(1, std::min<int64_t>({8, (2 * (int64_t)sms) / B, f.LE / 256}));
+  }
+  return launch_pdl(k_merge, dim3(B, n_split), dim3(256), 0, st, in, n_lists, qstride, lstride, list_len, k, out,
+                    set_thr, lower, f, bump, reset_lower ? 1 : 0, x, split_cnt);
 }
 
 // Grid (B, ceil(LE / 256)): every CTA recomputes its query's k weights (k <= 256

@@ -86,7 +86,9 @@ cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride
                          int k, uint64_t* out, cudaStream_t st, unsigned long long* set_thr = nullptr,
                          unsigned long long* lower = nullptr, const FinalizeArgs* fin = nullptr,
                          int list_len = -1, unsigned* bump = nullptr, bool reset_lower = false,
-                         const PeerXchg* px = nullptr);
+                         const PeerXchg* px = nullptr, unsigned* split_cnt = nullptr);
+// (split_cnt: [B] zeroed counters; when given with a prediction to compute, the merge runs
+// as (B, n_split) CTAs that split the finalize's columns -- see k_merge)
 
 // S6 + S7 as a separate kernel (tree search path with world == 1).
 cudaError_t launch_finalize(const uint64_t* top, int B, int k, const FinalizeArgs& f, cudaStream_t st);

@@ -222,7 +222,9 @@ __device__ __forceinline__ void merge_query(const uint64_t* __restrict__ in, int
                                             unsigned long long* __restrict__ set_thr,
                                             unsigned long long* __restrict__ lower, const FinalizeArgs& fin,
                                             int reset_lower, const PeerXchg* px, int t, Bar bar,
-                                            MergeScratch& S) {
+                                            MergeScratch& S, int64_t j0 = 0, int64_t j1 = -1,
+                                            bool primary = true, unsigned* split_cnt = nullptr,
+                                            int n_split = 1) {
   const int warp = t >> 5, lane = t & 31;
   const uint64_t* base = in + (int64_t)b * qstride;
   const int nch = (list_len + 31) >> 5;
@@ -230,7 +232,12 @@ __device__ __forceinline__ void merge_query(const uint64_t* __restrict__ in, int
   uint64_t lb = lower ? lower[b] : 0ull;
   if (t == 0) S.cnt = 0;
   bar();  // every thread has read lb; cnt is zero
-  if (lower && reset_lower && t == 0) lower[b] = 0ull;  // the next chunk's scan starts from no threshold
+  // the next chunk's scan starts from no threshold: reset once every column split of this
+  // query has read it (the last of n_split CTAs to arrive)
+  if (lower && reset_lower && t == 0) {
+    if (n_split <= 1) lower[b] = 0ull;
+    else if (atomicAdd(split_cnt + b, 1u) == (unsigned)n_split - 1) { lower[b] = 0ull; split_cnt[b] = 0u; }
+  }
   if (lb == 0) lb = 1;  // sentinel keys (0) never count
   // the lists of one query are usually contiguous (lstride == list_len): flat key f is base[f]
   const bool contiguous = lstride == (int64_t)list_len;
@@ -385,13 +392,13 @@ __device__ __forceinline__ void merge_query(const uint64_t* __restrict__ in, int
     for (int i = t; i < nout; i += kMergeThreads) S.topk[i] = S.cand[i];
   }
   bar();
-  for (int i = t; i < k; i += kMergeThreads) {
+  for (int i = t; primary && i < k; i += kMergeThreads) {
     const uint64_t v = i < nout ? S.topk[i] : 0ull;
     out[(int64_t)b * k + i] = v;
     if (px && px->G > 0 && px->key_dst[0])  // fused exchange 1: straight into every rank's gathered slot
       for (int g = 0; g < px->G; ++g) px->key_dst[g][(int64_t)b * k + i] = v;
   }
-  if (set_thr && t == 0) {
+  if (set_thr && primary && t == 0) {
     // seeding: the k-th best key of a subset of rows, minus one (strict lower bound,
     // the subset's own rows stay admissible in the full scan)
     const uint64_t kth = k <= nout ? S.topk[k - 1] : 0ull;
@@ -401,7 +408,7 @@ __device__ __forceinline__ void merge_query(const uint64_t* __restrict__ in, int
     if (nout < k)
       for (int i = nout + t; i < k; i += kMergeThreads) S.topk[i] = 0ull;
     bar();
-    finalize_query(S.topk, k, b, fin, 0, fin.LE, true, t, bar, S);
+    finalize_query(S.topk, k, b, fin, j0, j1 < 0 ? fin.LE : j1, primary, t, bar, S);
   }
 }
 

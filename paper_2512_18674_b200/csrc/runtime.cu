@@ -132,6 +132,7 @@ struct remoe_sps {
   uint64_t* local_top = nullptr;
   uint64_t* gathered = nullptr;    // [world][max_batch][max_k] (world > 1)
   uint64_t* global_top = nullptr;
+  unsigned* split_cnt = nullptr;   // [max_batch] column-split counters of the merge (zeroed, self-resetting)
   float* part = nullptr;           // [max_batch][LE] this rank's partial prediction (world > 1)
   float* part_all = nullptr;       // gathered partials / all-to-all receive buffer (world > 1)
   size_t part_all_floats = 0;
@@ -509,6 +510,8 @@ static remoe_status_t build_local(remoe_sps* h, const uint16_t* emb, const float
   ST_TRY(h->alloc((void**)&h->lists, (size_t)mb * lists_max * c.max_k * 8));
   ST_TRY(h->alloc((void**)&h->local_top, (size_t)mb * c.max_k * 8));
   ST_TRY(h->alloc((void**)&h->global_top, (size_t)mb * c.max_k * 8));
+  ST_TRY(h->alloc((void**)&h->split_cnt, (size_t)mb * sizeof(unsigned)));
+  CUDA_TRY(cudaMemsetAsync(h->split_cnt, 0, (size_t)mb * sizeof(unsigned), st));
   if (c.world > 1) {
     // exchange workspaces: keys [G][mb][max_k]; this rank's partial P
     // [mb][LE]; the gathered partials [G][mb][LE] when they fit xchg_ag_max, and always
@@ -831,7 +834,8 @@ static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k,
   // final k-th best key (every published value is some state's own k-th best or a
   // seeded strict bound), so the merge drops every key below it.
   const cudaError_t me = remoe::launch_merge(h->lists, bc, grid, (int64_t)grid * k, k, k, h->local_top, st, nullptr,
-                                             h->gthr, fin, -1, su.store ? h->seed_store.epoch : nullptr, true, px);
+                                             h->gthr, fin, -1, su.store ? h->seed_store.epoch : nullptr, true, px,
+                                             h->split_cnt);
   if (me != cudaSuccess) {
     // nothing resets the thresholds / retires the published seed keys now: do it here, so a
     // later chunk starts clean

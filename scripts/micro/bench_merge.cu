@@ -41,21 +41,23 @@ int main(int argc, char** argv) {
   cudaMalloc(&d_pred, (size_t)B * LE * 4); cudaMalloc(&d_sc, (size_t)B * k * 4); cudaMalloc(&d_ids, (size_t)B * k * 8);
   cudaStream_t st; cudaStreamCreate(&st);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  for (int variant = 0; variant < 4; ++variant) {
-    const bool use_lb = variant & 1, use_fin = variant & 2;
+  unsigned* d_split; cudaMalloc(&d_split, B * 4); cudaMemset(d_split, 0, B * 4);
+  for (int variant = 0; variant < 8; ++variant) {
+    const bool use_lb = variant & 1, use_fin = variant & 2, use_split = variant & 4;
+    if (use_split && !use_fin) continue;
     remoe::FinalizeArgs f{d_act, 0, N, 0, LE, 1.f, d_ids, d_sc, d_pred};
     float best = 1e9;
     for (int rep = 0; rep < 50; ++rep) {
       if (use_lb) cudaMemcpyAsync(d_lb, lb.data(), B * 8, cudaMemcpyHostToDevice, st);
       cudaEventRecord(e0, st);
       remoe::launch_merge(d_in, B, L, (int64_t)L * k, k, k, d_out, st, nullptr, use_lb ? d_lb : nullptr,
-                          use_fin ? &f : nullptr, k, nullptr, false);
+                          use_fin ? &f : nullptr, k, nullptr, use_lb, nullptr, use_split ? d_split : nullptr);
       cudaEventRecord(e1, st);
       cudaStreamSynchronize(st);
       float ms; cudaEventElapsedTime(&ms, e0, e1);
       best = std::min(best, ms);
     }
-    printf("B=%d L=%d k=%d LE=%d lower=%d finalize=%d: best %.2f us (%s)\n", B, L, k, LE, use_lb, use_fin, best * 1e3,
+    printf("B=%d L=%d k=%d LE=%d lower=%d finalize=%d split=%d: best %.2f us (%s)\n", B, L, k, LE, use_lb, use_fin, use_split, best * 1e3,
            cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
