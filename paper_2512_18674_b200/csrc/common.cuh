@@ -238,19 +238,27 @@ struct LaneTopk {
   // The sort network is sized to the lane's fill, not to CAP: with seeded thresholds a
   // buffer usually holds a handful of keys, and sorting all CAP = 512 slots of 32 lanes
   // one after another cost ~0.5 ms per scan at k = 128.
-  __device__ __forceinline__ void flush(uint64_t* my_out, int k) {
+  // scratch (optional): 32 keys of shared memory private to this lane -- a buffer in global
+  // memory (k > 32 with large CAP) is then sorted there instead of in place: the in-place
+  // insertion sort's dependent global loads and stores cost ~20-30 us per k = 64/128 scan.
+  __device__ __forceinline__ void flush(uint64_t* my_out, int k, uint64_t* scratch = nullptr) {
     const int lane = threadIdx.x & 31;
     // lanes holding at most 32 keys sort their own buffer (insertion sort, all lanes at
     // once) and write their list themselves; only fuller buffers take the warp network
     const bool self = my_out != nullptr && cnt <= 32;
     if (self) {
-      for (int i = 1; i < cnt; ++i) {
-        const uint64_t x = buf[i];
-        int j = i - 1;
-        while (j >= 0 && buf[j] < x) { buf[j + 1] = buf[j]; --j; }
-        buf[j + 1] = x;
+      uint64_t* sb = buf;
+      if (scratch) {
+        for (int i = 0; i < cnt; ++i) scratch[i] = buf[i];  // independent loads, in flight together
+        sb = scratch;
       }
-      for (int i = 0; i < k; ++i) my_out[i] = i < cnt ? buf[i] : 0ull;
+      for (int i = 1; i < cnt; ++i) {
+        const uint64_t x = sb[i];
+        int j = i - 1;
+        while (j >= 0 && sb[j] < x) { sb[j + 1] = sb[j]; --j; }
+        sb[j + 1] = x;
+      }
+      for (int i = 0; i < k; ++i) my_out[i] = i < cnt ? sb[i] : 0ull;
     }
     const unsigned rest = __ballot_sync(kFull, my_out != nullptr && !self);
     for (int L = 0; L < 32; ++L) {

@@ -346,8 +346,17 @@ __global__ void __launch_bounds__(kPThreads, 1)
     } else {
       uint64_t* out = active ? p.out + ((size_t)(qrow0 + m) * npl + (size_t)pair * 2 + parity) * (size_t)p.k
                              : nullptr;
-      if constexpr (KR > 0) tk.flush(out);
-      else tk.flush(out, p.k);
+      if constexpr (KR > 0) {
+        tk.flush(out);
+      } else {
+        // buffers in global memory: sort in the idle stage ring (see k_scan_tc)
+        uint64_t* scratch = nullptr;
+        if (!p.smem_bufs && (size_t)NST * kBox >= (size_t)kPEpiWarps * 32 * 32 * 8) {
+          asm volatile("bar.sync 2, %0;" ::"n"(kPEpiWarps * 32) : "memory");
+          scratch = reinterpret_cast<uint64_t*>(sA) + (size_t)slot * 32;
+        }
+        tk.flush(out, p.k, scratch);
+      }
     }
   }
   __syncthreads();

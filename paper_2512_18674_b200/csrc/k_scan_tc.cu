@@ -781,8 +781,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
       uint64_t* out =
           active ? out_sl + (((size_t)m * gridDim.x + blockIdx.x) * 2 + parity) * (size_t)p.k : nullptr;
-      if constexpr (KR > 0) tk.flush(out);
-      else tk.flush(out, p.k);
+      if constexpr (KR > 0) {
+        tk.flush(out);
+      } else {
+        // buffers in global memory: sort in the (now idle) TMA ring, 32 keys per lane --
+        // once every epilogue warp consumed its last accumulator, every MMA has read the ring
+        uint64_t* scratch = nullptr;
+        if (!p.smem_bufs && (size_t)NST * kStageBytes >= (size_t)kEpiWarps * 32 * 32 * 8) {
+          asm volatile("bar.sync 2, %0;" ::"n"(kEpiWarps * 32) : "memory");
+          scratch = reinterpret_cast<uint64_t*>(sB) + (size_t)slot * 32;
+        }
+        tk.flush(out, p.k, scratch);
+      }
     }
   }
   __syncthreads();
