@@ -859,7 +859,7 @@ static remoe_status_t stage_merge(remoe_sps* h, int bc, int k, int64_t* ids, flo
   const remoe::FinalizeArgs f{h->act, c.global_offset, c.n_local, 2, h->LE, c.temperature, ids, scores,
                               want_pred ? h->part : nullptr};
   CUDA_TRY(remoe::launch_merge(h->gathered, bc, c.world, k, (int64_t)bc * k, k, h->global_top, st, nullptr,
-                               nullptr, &f));
+                               nullptr, &f, -1, nullptr, false, nullptr, h->split_cnt));
   ++*launches;
   return REMOE_OK;
 }
