@@ -229,6 +229,20 @@ __device__ __forceinline__ void merge_query(const uint64_t* __restrict__ in, int
   const uint64_t* base = in + (int64_t)b * qstride;
   const int nch = (list_len + 31) >> 5;
   const int items = n_lists * nch;
+  // Short contiguous lists (<= 32 keys each, <= 8 keys per thread in all): ONE round trip --
+  // every key of the query is loaded here, together with lb, and the list heads (key f is
+  // the head of list f / list_len when f % list_len == 0) come from the same registers.
+  const int64_t n_keys = (int64_t)n_lists * list_len;
+  const bool one_trip = nch == 1 && lstride == (int64_t)list_len && n_keys <= 8 * kMergeThreads &&
+                        n_lists >= k && n_lists <= kSelCap;
+  uint64_t kk1[8];
+  if (one_trip) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int f = t + kMergeThreads * u;
+      kk1[u] = f < n_keys ? __ldcg(base + f) : 0ull;
+    }
+  }
   uint64_t lb = lower ? lower[b] : 0ull;
   if (t == 0) S.cnt = 0;
   bar();  // every thread has read lb; cnt is zero
@@ -249,7 +263,6 @@ __device__ __forceinline__ void merge_query(const uint64_t* __restrict__ in, int
   };
   // flat key f = l * list_len + i: the whole block reads 8 keys per thread per round
   // (one L2 round trip per 2048 keys, instead of one per 32 lists of a warp)
-  const int64_t n_keys = (int64_t)n_lists * list_len;
   auto flat_key = [&](int64_t f) -> uint64_t {
     if (f >= n_keys) return 0ull;
     if (contiguous) return __ldcg(base + f);
@@ -310,7 +323,15 @@ __device__ __forceinline__ void merge_query(const uint64_t* __restrict__ in, int
   // a much tighter bound than lb when the state lists are many (S4: 1 or 2 per CTA).
   if (n_lists >= k && n_lists <= kSelCap) {
     if (t == 0) S.prefix = 0ull;
-    for (int l = t; l < n_lists; l += kMergeThreads) S.cand[l] = __ldcg(base + (int64_t)l * lstride);
+    if (one_trip) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int f = t + kMergeThreads * u;
+        if (f < n_keys && f % list_len == 0) S.cand[f / list_len] = kk1[u];
+      }
+    } else {
+      for (int l = t; l < n_lists; l += kMergeThreads) S.cand[l] = __ldcg(base + (int64_t)l * lstride);
+    }
     bar();
     for (int i = t; i < n_lists; i += kMergeThreads) {
       const uint64_t x = S.cand[i];
@@ -323,8 +344,14 @@ __device__ __forceinline__ void merge_query(const uint64_t* __restrict__ in, int
     if (S.prefix > lb) lb = S.prefix;
     bar();
   }
-  if (nch >= 2 && nch <= 8 && (int64_t)n_lists * nch <= kItemCap) collect_lists(lb);
-  else collect(lb);
+  if (one_trip) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) append(kk1[u], lb);  // the keys are already in registers
+  } else if (nch >= 2 && nch <= 8 && (int64_t)n_lists * nch <= kItemCap) {
+    collect_lists(lb);
+  } else {
+    collect(lb);
+  }
   bar();
   int n = S.cnt;
   if (n > kSelCap) {
