@@ -88,8 +88,11 @@ cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride
   // column splits of the finalize: ~2 CTAs per SM in total, >= 256 columns per split
   int n_split = 1;
   if (split_cnt && fin && f.pred && f.n_pred_peer == 0 && x.G == 0 && !set_thr) {
-    static int sms = 0;
-    if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0) != cudaSuccess) { cudaGetLastError(); sms = 148; }
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+      cudaGetLastError();
+      sms = 148;
+    }
     n_split = (int)std::max<int64_t>(1, std::min<int64_t>({8, (2 * (int64_t)sms) / B, f.LE / 256}));
   }
   return launch_pdl(k_merge, dim3(B, n_split), dim3(256), 0, st, in, n_lists, qstride, lstride, list_len, k, out,
