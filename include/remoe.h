@@ -264,7 +264,9 @@ REMOE_API remoe_status_t remoe_sps_tree_query(remoe_sps_t h, const uint16_t* q_b
  * the receive buffers are mapped through CUDA IPC (NVLink peer access on one node; the
  * ranks agree at build, and all fall back to NCCL if any cannot map its peers); in a
  * loopback group they are the members' own buffers.  remoe_sps_get_info reports which
- * path a handle uses (fused_exchange).
+ * path a handle uses (fused_exchange).  The chunk sequence numbers live on the device, so
+ * fused multi-rank queries (all-gather layout, B <= max_batch) are captured once as a CUDA
+ * graph per buffer set and replayed, like one-GPU queries; loopback group queries too.
  */
 REMOE_API remoe_status_t remoe_loopback_group_create(int32_t world, remoe_group_t* out);
 REMOE_API remoe_status_t remoe_loopback_group_destroy(remoe_group_t g);

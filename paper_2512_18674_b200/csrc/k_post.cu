@@ -54,6 +54,15 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
                                                PeerXchg px, unsigned* __restrict__ split_cnt) {
   __shared__ MergeScratch S;
   pdl_wait();  // the scan's lists and thresholds
+  if (px.G > 0 && px.seq_ptr) {  // the chunk's sequence number and buffer parity, on the device
+    px.seq = *px.seq_ptr + 1;
+    if (px.seq & 1) {
+      in += px.in_par;
+      for (int g = 0; g < px.G; ++g)
+        if (px.key_dst[g]) px.key_dst[g] += px.key_par;
+      for (int g = 0; g < fin.n_pred_peer; ++g) fin.pred_peer[g] += px.pred_par;
+    }
+  }
   // (key loads are ld.global.cg: L2-coherent, so keys a peer stored over NVLink during
   // this kernel's lifetime -- fused exchange 1 -- are never read through a stale L1 line)
   if (px.G > 0 && px.wait_flags) peer_wait(px.wait_flags, px.G, px.seq);  // fused exchange 1: every rank's keys
@@ -124,8 +133,13 @@ cudaError_t launch_finalize(const uint64_t* top, int B, int k, const FinalizeArg
 // the same gathered partials in the same order, so all ranks (and every batch position)
 // get identical bits (ncclAllReduce's ring order would not guarantee that).
 __global__ void k_psum(const float* parts, int G, int64_t stride, int64_t n, float* __restrict__ out,
-                       const unsigned long long* __restrict__ wait_flags, unsigned long long seq) {
+                       const unsigned long long* __restrict__ wait_flags, unsigned long long seq,
+                       const unsigned long long* __restrict__ seq_ptr, int64_t parts_par) {
   pdl_wait();
+  if (seq_ptr) {
+    seq = *seq_ptr + 1;
+    if (seq & 1) parts += parts_par;
+  }
   if (wait_flags) peer_wait(wait_flags, G, seq);  // fused exchange 2: every rank's partial landed
   const int64_t step = (int64_t)gridDim.x * blockDim.x;
   if ((stride & 3) == 0 && (n & 3) == 0 && ((reinterpret_cast<uintptr_t>(parts) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
@@ -147,13 +161,24 @@ __global__ void k_psum(const float* parts, int G, int64_t stride, int64_t n, flo
 }
 
 cudaError_t launch_psum(const float* parts, int G, int64_t part_stride, int64_t n, float* out, cudaStream_t st,
-                        const unsigned long long* wait_flags, unsigned long long seq) {
+                        const unsigned long long* wait_flags, unsigned long long seq,
+                        const unsigned long long* seq_ptr, int64_t parts_par) {
   if (n <= 0) return cudaSuccess;
   const int64_t units = (n + 3) / 4;
   const unsigned grid = (unsigned)std::min<int64_t>((units + 255) / 256, 148 * 8);
   cudaError_t e = set_smem_attrs_once((const void*)k_psum, 0);
   if (e != cudaSuccess) return e;
-  return launch_pdl(k_psum, dim3(grid), dim3(256), 0, st, parts, G, part_stride, n, out, wait_flags, seq);
+  return launch_pdl(k_psum, dim3(grid), dim3(256), 0, st, parts, G, part_stride, n, out, wait_flags, seq, seq_ptr,
+                    parts_par);
+}
+
+__global__ void k_seq_bump(unsigned long long* seq) {
+  pdl_wait();
+  *seq += 1ull;
+}
+
+cudaError_t launch_seq_bump(unsigned long long* seq, cudaStream_t st) {
+  return launch_pdl(k_seq_bump, dim3(1), dim3(1), 0, st, seq);
 }
 
 // ---------------------------------------------------------------- S8 plan

@@ -70,7 +70,13 @@ struct PeerXchg {
   unsigned long long* flag_dst[kMaxPeers];   // this rank's flag in rank g (null: no signal)
   unsigned* counter;                         // finished CTAs (the last one signals, resets it)
   const unsigned long long* wait_flags;      // [G] flags to wait for before reading (or null)
-  unsigned long long seq;
+  unsigned long long seq;                    // the chunk's sequence number (when seq_ptr is null)
+  // Graph-replayable form: the chunk's sequence number is read on the device (*seq_ptr + 1;
+  // k_seq_bump advances it after the chunk), and odd chunks use the parity-1 halves of the
+  // double-buffered receive buffers: input lists at in + in_par, key_dst[g] + key_par,
+  // the partial rows at fin.pred_peer[g] + pred_par.
+  const unsigned long long* seq_ptr;
+  int64_t in_par, key_par, pred_par;
 };
 
 // S4 / S5: per query, merge n_lists sorted key lists of length list_len (default k) into
@@ -95,9 +101,13 @@ cudaError_t launch_finalize(const uint64_t* top, int B, int k, const FinalizeArg
 
 // Multi-GPU S7 combine: out[i] = sum_{g = 0..G-1} parts[g * part_stride + i] for i < n, g
 // ascending (a fixed order: every rank and every batch position gets the same bits).
-// wait_flags (fused exchange 2): first wait until wait_flags[g] >= seq for every g < G.
+// wait_flags (fused exchange 2): first wait until wait_flags[g] >= seq for every g < G;
+// with seq_ptr, seq = *seq_ptr + 1 and odd chunks read parts + parts_par.
 cudaError_t launch_psum(const float* parts, int G, int64_t part_stride, int64_t n, float* out, cudaStream_t st,
-                        const unsigned long long* wait_flags = nullptr, unsigned long long seq = 0);
+                        const unsigned long long* wait_flags = nullptr, unsigned long long seq = 0,
+                        const unsigned long long* seq_ptr = nullptr, int64_t parts_par = 0);
+// *seq += 1 (one thread): ends a fused-exchange chunk (graph-replayable sequence numbers).
+cudaError_t launch_seq_bump(unsigned long long* seq, cudaStream_t st);
 
 // S8: cold mask of the n_cold smallest entries per (query, layer).
 cudaError_t launch_plan(const float* pred, int B, int L, int E, int n_cold, uint8_t* mask,

@@ -108,6 +108,29 @@ struct remoe_sps;
 struct remoe_group {
   int world = 0;
   std::vector<remoe_sps*> members;  // by rank; nullptr until that rank is built
+  // CUDA graphs of whole group queries (fused exchange only: every step is a kernel), keyed
+  // by the buffers; dropped when a member is destroyed
+  struct Graph {
+    const void* q = nullptr;
+    std::vector<const void*> bufs;
+    int B = -1, k = -1;
+    cudaGraphExec_t exec = nullptr;
+    int launches = 0;
+  };
+  std::vector<Graph> graphs;
+  cudaStream_t gst = nullptr;
+  cudaEvent_t gev = nullptr, gev_done = nullptr;
+  void reset_graphs() {
+    for (Graph& gr : graphs)
+      if (gr.exec) cudaGraphExecDestroy(gr.exec);
+    graphs.clear();
+  }
+  ~remoe_group() {
+    reset_graphs();
+    if (gev) cudaEventDestroy(gev);
+    if (gev_done) cudaEventDestroy(gev_done);
+    if (gst) cudaStreamDestroy(gst);
+  }
 };
 
 struct remoe_sps {
@@ -142,7 +165,7 @@ struct remoe_sps {
   bool fused = false;
   unsigned long long* xflag = nullptr;  // [2][world]: exchange-1 / exchange-2 flag of each rank
   unsigned* xcount = nullptr;           // [2] finished-CTA counters of the two producing kernels
-  unsigned long long xseq = 0;          // chunks exchanged so far (identical on every rank)
+  unsigned long long* d_xseq = nullptr; // chunks exchanged so far, on the device (identical on every rank)
   uint64_t* p_gathered[remoe::kMaxPeers] = {};
   float* p_part_all[remoe::kMaxPeers] = {};
   unsigned long long* p_xflag[remoe::kMaxPeers] = {};
@@ -293,6 +316,7 @@ struct remoe_sps {
     if (group) {
       if (cfg.rank >= 0 && cfg.rank < (int)group->members.size() && group->members[cfg.rank] == this)
         group->members[cfg.rank] = nullptr;
+      group->reset_graphs();  // captured with this member's buffers
       group = nullptr;
     }
   }
@@ -528,6 +552,8 @@ static remoe_status_t build_local(remoe_sps* h, const uint16_t* emb, const float
     if (h->fused) {
       ST_TRY(h->alloc((void**)&h->xflag, 2 * G * sizeof(unsigned long long)));
       ST_TRY(h->alloc((void**)&h->xcount, 2 * sizeof(unsigned)));
+      ST_TRY(h->alloc((void**)&h->d_xseq, sizeof(unsigned long long)));
+      CUDA_TRY(cudaMemsetAsync(h->d_xseq, 0, sizeof(unsigned long long), st));
       CUDA_TRY(cudaMemsetAsync(h->xflag, 0, 2 * G * sizeof(unsigned long long), st));
       CUDA_TRY(cudaMemsetAsync(h->xcount, 0, 2 * sizeof(unsigned), st));
     }
@@ -969,23 +995,25 @@ static remoe_status_t exchange(remoe_sps* const* hs, int nh, Xchg x, int bc, int
   return REMOE_OK;
 }
 
-// Fused exchange (h->fused): this chunk's parity buffers and the PeerXchg of
-// each producing kernel.  Exchange 1: the S4 merge stores the local keys into every rank's
-// gathered[par][rank]; exchange 2 (all-gather layout): the S5 merge stores the partial rows
-// into every rank's part_all[par][rank]; each raises this rank's flag to xseq in every rank.
-static size_t gathered_par(const remoe_sps* h) {
-  return (size_t)(h->xseq & 1) * h->cfg.world * h->cfg.max_batch * h->cfg.max_k;
+// Fused exchange (h->fused): the PeerXchg of each producing kernel.  Exchange 1:
+// the S4 merge stores the local keys into every rank's gathered[par][rank]; exchange 2
+// (all-gather layout): the S5 merge stores the partial rows into every rank's
+// part_all[par][rank]; each raises this rank's flag in every rank.  The chunk's sequence
+// number (and with it the parity par) is read on the device from d_xseq and advanced by
+// k_seq_bump after the chunk, so the whole sequence can be captured once in a CUDA graph.
+static size_t gathered_par_stride(const remoe_sps* h) {
+  return (size_t)h->cfg.world * h->cfg.max_batch * h->cfg.max_k;
 }
-static size_t part_all_par(const remoe_sps* h) { return (size_t)(h->xseq & 1) * h->part_all_floats; }
 static remoe::PeerXchg fused_keys(const remoe_sps* h, int bc, int k) {
   remoe::PeerXchg px{};
   px.G = h->cfg.world;
   for (int g = 0; g < px.G; ++g) {
-    px.key_dst[g] = h->p_gathered[g] + gathered_par(h) + (size_t)h->cfg.rank * bc * k;
-    px.flag_dst[g] = h->p_xflag[g] + h->cfg.rank;  // exchange-1 flags: [0, G)
+    px.key_dst[g] = h->p_gathered[g] + (size_t)h->cfg.rank * bc * k;  // parity 0 (key_par: parity 1)
+    px.flag_dst[g] = h->p_xflag[g] + h->cfg.rank;                     // exchange-1 flags: [0, G)
   }
   px.counter = h->xcount;
-  px.seq = h->xseq;
+  px.seq_ptr = h->d_xseq;
+  px.key_par = (int64_t)gathered_par_stride(h);
   return px;
 }
 static remoe_status_t stage_merge_fused(remoe_sps* h, int bc, int k, int64_t* ids, float* scores, bool want_pred,
@@ -996,17 +1024,19 @@ static remoe_status_t stage_merge_fused(remoe_sps* h, int bc, int k, int64_t* id
   remoe::PeerXchg px{};
   px.G = c.world;
   px.wait_flags = h->xflag;  // every rank's exchange-1 flag
-  px.seq = h->xseq;
+  px.seq_ptr = h->d_xseq;
+  px.in_par = (int64_t)gathered_par_stride(h);
   if (want_pred && ag) {
     f.n_pred_peer = c.world;
     for (int g = 0; g < c.world; ++g) {
-      f.pred_peer[g] = h->p_part_all[g] + part_all_par(h) + (size_t)c.rank * bc * h->LE;
-      px.flag_dst[g] = h->p_xflag[g] + c.world + c.rank;  // exchange-2 flags: [G, 2G)
+      f.pred_peer[g] = h->p_part_all[g] + (size_t)c.rank * bc * h->LE;  // parity 0 (pred_par: parity 1)
+      px.flag_dst[g] = h->p_xflag[g] + c.world + c.rank;                 // exchange-2 flags: [G, 2G)
     }
     px.counter = h->xcount + 1;
+    px.pred_par = (int64_t)h->part_all_floats;
   }
-  CUDA_TRY(remoe::launch_merge(h->gathered + gathered_par(h), bc, c.world, k, (int64_t)bc * k, k, h->global_top,
-                               st, nullptr, nullptr, &f, -1, nullptr, false, &px));
+  CUDA_TRY(remoe::launch_merge(h->gathered, bc, c.world, k, (int64_t)bc * k, k, h->global_top, st, nullptr, nullptr,
+                               &f, -1, nullptr, false, &px));
   ++*launches;
   return REMOE_OK;
 }
@@ -1023,23 +1053,30 @@ static remoe_status_t query_ranks(remoe_sps* const* hs, int nh, int bc, int k, i
   const bool want = pred != nullptr && pred[0] != nullptr;
   const bool ag = xchg_allgather(hs[0], bc);
   if (fusable && hs[0]->fused) {
-    for (int i = 0; i < nh; ++i) ++hs[i]->xseq;  // identical on every rank (same chunk sequence)
+    auto bump = [&]() -> remoe_status_t {  // the chunk is over on this rank: advance its sequence
+      for (int i = 0; i < nh; ++i) {
+        CUDA_TRY(remoe::launch_seq_bump(hs[i]->d_xseq, st));
+        ++*launches;
+      }
+      return REMOE_OK;
+    };
     for (int i = 0; i < nh; ++i) {
       const remoe::PeerXchg px = fused_keys(hs[i], bc, k);
       ST_TRY(local(hs[i], &px));
     }
     for (int i = 0; i < nh; ++i) ST_TRY(stage_merge_fused(hs[i], bc, k, ids[i], scores[i], want, ag, st, launches));
-    if (!want) return REMOE_OK;
+    if (!want) return bump();
     if (ag) {
       for (int i = 0; i < nh; ++i) {
         remoe_sps* h = hs[i];
-        CUDA_TRY(remoe::launch_psum(h->part_all + part_all_par(h), h->cfg.world, (int64_t)bc * h->LE,
-                                    (int64_t)bc * h->LE, pred[i], st, h->xflag + h->cfg.world, h->xseq));
+        CUDA_TRY(remoe::launch_psum(h->part_all, h->cfg.world, (int64_t)bc * h->LE, (int64_t)bc * h->LE, pred[i], st,
+                                    h->xflag + h->cfg.world, 0, h->d_xseq, (int64_t)h->part_all_floats));
         ++*launches;
       }
-      return REMOE_OK;
+      return bump();
     }
     // all-to-all layout: the partials (h->part) go through the collectives below
+    ST_TRY(bump());
   } else {
     for (int i = 0; i < nh; ++i) ST_TRY(local(hs[i], nullptr));
     ST_TRY(exchange(hs, nh, Xchg::Keys, bc, k, pred, st));
@@ -1148,7 +1185,10 @@ remoe_status_t remoe_sps_query(remoe_sps_t h, const uint16_t* q, int32_t B, int3
   NvtxRange nr("remoe_sps_query");
   cudaStream_t st = (cudaStream_t)stream;
   const int mb = h->cfg.max_batch;
-  if (B <= mb && h->cfg.world == 1 && !h->prof && h->use_graphs)
+  // one GPU, or world > 1 with the fused exchange in the all-gather layout (every step of
+  // the chunk is then a kernel of this library -- no NCCL call -- and graph-capturable)
+  const bool graphable = h->cfg.world == 1 || (h->fused && !h->group && (!pred || xchg_allgather(h, B)));
+  if (B <= mb && graphable && !h->prof && h->use_graphs)
     return query_device_graph(h, q, B, k, ids, scores, pred, st);
   int launches = 0;
   for (int b0 = 0; b0 < B; b0 += mb) {
@@ -1195,6 +1235,60 @@ remoe_status_t remoe_sps_query_group(remoe_group_t g, const uint16_t* q, int32_t
   const int mb = hs[0]->cfg.max_batch;
   const int64_t LE = hs[0]->LE;
   int launches = 0;
+  if (B <= mb && hs[0]->fused && (!want || xchg_allgather(hs[0], B)) && hs[0]->use_graphs && !hs[0]->prof) {
+    // the whole G-rank sequence as one cached CUDA graph (replayed on the group's stream,
+    // ordered after the caller's earlier work and before its later work by two events)
+    if (!g->gst) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&g->gst, cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&g->gev, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&g->gev_done, cudaEventDisableTiming));
+    }
+    std::vector<const void*> bufs;
+    for (int r = 0; r < G; ++r) {
+      bufs.push_back(ids[r]);
+      bufs.push_back(scores[r]);
+      bufs.push_back(want ? pred[r] : nullptr);
+    }
+    remoe_group::Graph* gr = nullptr;
+    for (auto& e : g->graphs)
+      if (e.exec && e.q == q && e.B == B && e.k == k && e.bufs == bufs) { gr = &e; break; }
+    CUDA_TRY(cudaEventRecord(g->gev, st));
+    CUDA_TRY(cudaStreamWaitEvent(g->gst, g->gev, 0));
+    if (!gr) {
+      if (g->graphs.size() >= 8) g->reset_graphs();
+      g->graphs.emplace_back();
+      gr = &g->graphs.back();
+      CUDA_TRY(cudaStreamBeginCapture(g->gst, cudaStreamCaptureModeRelaxed));
+      int nl = 0;
+      std::vector<float*> pc(G);
+      for (int r = 0; r < G; ++r) pc[r] = want ? pred[r] : nullptr;
+      const remoe_status_t qs = query_ranks(
+          hs, G, B, k, ids, scores, want ? pc.data() : nullptr, g->gst, &nl,
+          [&](remoe_sps* hh, const remoe::PeerXchg* px) { return stage_scan(hh, q, B, k, nullptr, g->gst, &nl, px); },
+          true);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(g->gst, &graph);
+      if (qs != REMOE_OK || ce != cudaSuccess || !graph) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        g->graphs.pop_back();
+        if (qs != REMOE_OK) return qs;
+        return fail(REMOE_ERR_CUDA, "group graph capture failed: %s", cudaGetErrorString(ce));
+      }
+      const cudaError_t ie = cudaGraphInstantiate(&gr->exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ie != cudaSuccess) {
+        g->graphs.pop_back();
+        return fail(REMOE_ERR_CUDA, "group graph instantiate: %s", cudaGetErrorString(ie));
+      }
+      gr->q = q; gr->bufs = bufs; gr->B = B; gr->k = k; gr->launches = nl;
+    }
+    CUDA_TRY(cudaGraphLaunch(gr->exec, g->gst));
+    CUDA_TRY(cudaEventRecord(g->gev_done, g->gst));
+    CUDA_TRY(cudaStreamWaitEvent(st, g->gev_done, 0));
+    for (int r = 0; r < G; ++r) hs[r]->last_launches = gr->launches;
+    return REMOE_OK;
+  }
   std::vector<int64_t*> ic(G);
   std::vector<float*> sc(G), pc(G);
   for (int b0 = 0; b0 < B; b0 += mb) {

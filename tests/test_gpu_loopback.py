@@ -197,6 +197,43 @@ def test_loopback_fused_exchange(G, xchg, monkeypatch):
     assert np.abs(pred[0] - p1).max() <= 1e-6
 
 
+@pytest.mark.parametrize("G", [2, 8])
+def test_loopback_fused_graph_replays(G, monkeypatch):
+    """Fused exchange with B <= max_batch: the whole G-rank query is captured once as a CUDA
+    graph and replayed; the chunk sequence numbers live on the device (k_seq_bump), so
+    replays alternate the double-buffer parity and keep advancing the flags.  Five replays
+    with the same buffers and one capture with new buffers all equal the collective path
+    bit for bit (ids, scores, pred); without pred the graph is the exchange-1 half."""
+    c, x, a = store(50_001)
+    B, k = 13, 10
+    qb = gen.queries(c.store_seed, c.query_seed, 50_001, c.dim, B, mode=1)
+    g0 = group(x, a, G, max_k=16, max_batch=16)
+    ref = run_group(g0, qb, k)
+    g0.close()
+    monkeypatch.setenv("REMOE_FUSED_COMM", "1")
+    g = group(x, a, G, max_k=16, max_batch=16)
+    q = torch.from_numpy(qb.view(np.int16)).cuda()
+    dev_ids = [torch.empty((B, k), dtype=torch.int64, device="cuda") for _ in range(G)]
+    dev_sc = [torch.empty((B, k), dtype=torch.float32, device="cuda") for _ in range(G)]
+    dev_pred = [torch.empty((B, c.layers, c.experts), dtype=torch.float32, device="cuda") for _ in range(G)]
+    for rep in range(6):  # the first call captures, the next five replay (same buffers)
+        for t in dev_ids + dev_sc + dev_pred:
+            t.zero_()
+        remoe.remoe_sps_query_group(g.group, q, B, k, dev_ids, dev_sc, dev_pred)
+        torch.cuda.synchronize()
+        ids = [t.cpu().numpy() for t in dev_ids]
+        sc = [t.cpu().numpy() for t in dev_sc]
+        pred = [t.cpu().numpy() for t in dev_pred]
+        for r in range(G):
+            assert np.array_equal(ids[r], ref[0][r]) and np.array_equal(sc[r], ref[1][r]), f"replay {rep} rank {r}"
+            assert np.array_equal(pred[r], ref[2][r]), f"replay {rep} rank {r}: pred"
+    ids2, sc2, _ = run_group(g, qb, k, want_pred=False)
+    for r in range(G):
+        assert np.array_equal(ids2[r], ref[0][r]) and np.array_equal(sc2[r], ref[1][r])
+    assert g.ranks[0].info().fused_exchange == 1
+    g.close()
+
+
 def test_loopback_errors():
     c, x, a = store(1_000, "tiny")
     gid = remoe.remoe_loopback_group_create(2)
