@@ -54,18 +54,21 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
                                                PeerXchg px, unsigned* __restrict__ split_cnt) {
   __shared__ MergeScratch S;
   pdl_wait();  // the scan's lists and thresholds
-  if (px.G > 0 && px.seq_ptr) {  // the chunk's sequence number and buffer parity, on the device
-    px.seq = *px.seq_ptr + 1;
-    if (px.seq & 1) {
+  // the chunk's sequence number and buffer parity, on the device (offsets, not edits of the
+  // pointer arrays: indexing a modified parameter array would move it to the local stack)
+  unsigned long long seq = px.seq;
+  int64_t key_off = 0, pred_off = 0;
+  if (px.G > 0 && px.seq_ptr) {
+    seq = *px.seq_ptr + 1;
+    if (seq & 1) {
       in += px.in_par;
-      for (int g = 0; g < px.G; ++g)
-        if (px.key_dst[g]) px.key_dst[g] += px.key_par;
-      for (int g = 0; g < fin.n_pred_peer; ++g) fin.pred_peer[g] += px.pred_par;
+      key_off = px.key_par;
+      pred_off = px.pred_par;
     }
   }
   // (key loads are ld.global.cg: L2-coherent, so keys a peer stored over NVLink during
   // this kernel's lifetime -- fused exchange 1 -- are never read through a stale L1 line)
-  if (px.G > 0 && px.wait_flags) peer_wait(px.wait_flags, px.G, px.seq);  // fused exchange 1: every rank's keys
+  if (px.G > 0 && px.wait_flags) peer_wait(px.wait_flags, px.G, seq);  // fused exchange 1: every rank's keys
   // the scan is complete: a new seeding epoch for the next chunk (stale published keys of
   // this one can never be taken for the next one's)
   if (bump && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(bump, 1u);
@@ -77,8 +80,8 @@ __global__ void __launch_bounds__(256) k_merge(const uint64_t* __restrict__ in, 
   const int64_t j0 = (int64_t)blockIdx.y * chunk;
   const int64_t j1 = j0 + chunk < fin.LE ? j0 + chunk : fin.LE;
   merge_query(in, blockIdx.x, n_lists, qstride, lstride, list_len, k, out, set_thr, lower, fin, reset_lower, &px,
-              threadIdx.x, [] { __syncthreads(); }, S, j0, j1, blockIdx.y == 0, split_cnt, n_split);
-  if (px.G > 0 && px.flag_dst[0]) peer_signal(px);
+              threadIdx.x, [] { __syncthreads(); }, S, j0, j1, blockIdx.y == 0, split_cnt, n_split, key_off, pred_off);
+  if (px.G > 0 && px.flag_dst[0]) peer_signal(px, seq);
 }
 
 cudaError_t launch_merge(const uint64_t* in, int B, int n_lists, int64_t qstride, int64_t lstride,

@@ -79,7 +79,7 @@ __device__ __forceinline__ void peer_wait(const unsigned long long* flags, int G
 }
 // Whole CTA, after its peer stores: the last CTA of the grid raises this rank's flag in
 // every rank (release, system scope) and resets the counter for the next exchange.
-__device__ __forceinline__ void peer_signal(const PeerXchg& px) {
+__device__ __forceinline__ void peer_signal(const PeerXchg& px, unsigned long long seq) {
   __threadfence_system();  // this CTA's peer stores before its arrival
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -88,7 +88,7 @@ __device__ __forceinline__ void peer_signal(const PeerXchg& px) {
       atomicExch(px.counter, 0u);
       __threadfence_system();  // every CTA's stores (seen through the counter) before the flags
       for (int g = 0; g < px.G; ++g)
-        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(px.flag_dst[g]), "l"(px.seq) : "memory");
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(px.flag_dst[g]), "l"(seq) : "memory");
     }
   }
 }
@@ -102,7 +102,7 @@ __device__ __forceinline__ void peer_signal(const PeerXchg& px) {
 template <class Bar>
 __device__ __forceinline__ void finalize_query(const uint64_t* tb, int k, int b, const FinalizeArgs& f,
                                                int64_t j0, int64_t j1, bool write_ids, int t, Bar bar,
-                                               MergeScratch& S) {
+                                               MergeScratch& S, int64_t pred_off = 0) {
   const int lane = t & 31, warp = t >> 5;
   const float s0 = key_score(tb[0]);
   float e = 0.f;
@@ -178,8 +178,8 @@ __device__ __forceinline__ void finalize_query(const uint64_t* tb, int k, int b,
         }
       }
       for (int o = 0; o < no; ++o) {
-        reinterpret_cast<float4*>(outs[o] + (int64_t)b * f.LE)[ca] = acc_a;
-        if (vb) reinterpret_cast<float4*>(outs[o] + (int64_t)b * f.LE)[cb] = acc_b;
+        reinterpret_cast<float4*>(outs[o] + pred_off + (int64_t)b * f.LE)[ca] = acc_a;
+        if (vb) reinterpret_cast<float4*>(outs[o] + pred_off + (int64_t)b * f.LE)[cb] = acc_b;
       }
     }
     return;
@@ -206,8 +206,8 @@ __device__ __forceinline__ void finalize_query(const uint64_t* tb, int k, int b,
       }
     }
     for (int o = 0; o < no; ++o) {
-      outs[o][(int64_t)b * f.LE + ja] = acc_a;
-      if (vb) outs[o][(int64_t)b * f.LE + jb] = acc_b;
+      outs[o][pred_off + (int64_t)b * f.LE + ja] = acc_a;
+      if (vb) outs[o][pred_off + (int64_t)b * f.LE + jb] = acc_b;
     }
   }
 }
@@ -224,7 +224,7 @@ __device__ __forceinline__ void merge_query(const uint64_t* __restrict__ in, int
                                             int reset_lower, const PeerXchg* px, int t, Bar bar,
                                             MergeScratch& S, int64_t j0 = 0, int64_t j1 = -1,
                                             bool primary = true, unsigned* split_cnt = nullptr,
-                                            int n_split = 1) {
+                                            int n_split = 1, int64_t key_off = 0, int64_t pred_off = 0) {
   const int warp = t >> 5, lane = t & 31;
   const uint64_t* base = in + (int64_t)b * qstride;
   const int nch = (list_len + 31) >> 5;
@@ -423,7 +423,7 @@ __device__ __forceinline__ void merge_query(const uint64_t* __restrict__ in, int
     const uint64_t v = i < nout ? S.topk[i] : 0ull;
     out[(int64_t)b * k + i] = v;
     if (px && px->G > 0 && px->key_dst[0])  // fused exchange 1: straight into every rank's gathered slot
-      for (int g = 0; g < px->G; ++g) px->key_dst[g][(int64_t)b * k + i] = v;
+      for (int g = 0; g < px->G; ++g) px->key_dst[g][key_off + (int64_t)b * k + i] = v;
   }
   if (set_thr && primary && t == 0) {
     // seeding: the k-th best key of a subset of rows, minus one (strict lower bound,
@@ -435,7 +435,7 @@ __device__ __forceinline__ void merge_query(const uint64_t* __restrict__ in, int
     if (nout < k)
       for (int i = nout + t; i < k; i += kMergeThreads) S.topk[i] = 0ull;
     bar();
-    finalize_query(S.topk, k, b, fin, j0, j1 < 0 ? fin.LE : j1, primary, t, bar, S);
+    finalize_query(S.topk, k, b, fin, j0, j1 < 0 ? fin.LE : j1, primary, t, bar, S, pred_off);
   }
 }
 
