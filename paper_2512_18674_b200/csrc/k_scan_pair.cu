@@ -70,7 +70,17 @@ struct PairArgs {
   int merge_in_cta;
   int dbg;                 // REMOE_TC_DBG experiment bits (wrong results): 128 = load the query
                            // box only for the first tile, 256 = the store box only for the first
+  // Group lockstep (REMOE_PAIR_LOCKSTEP=1, several query groups per launch): a pair starts
+  // loading tile round r only once the groups have issued round r - kLockWindow on average,
+  // so they read each store tile within a few rounds of each other and the later ones hit L2.
+  // Measured at c3 B = 1024 (4 groups): DRAM 1.03-1.05x the algorithmic bytes instead of
+  // 1.11-1.36x, but the scan ~2% slower (pairs wait for the slowest group; at 8 groups -8%,
+  // at a 6-round window the live set thrashes L2) -- off by default: time is the metric.
+  unsigned* prog;          // [gridDim.y] rounds issued per group (zeroed; reset by the last CTA)
+  unsigned* exit_cnt;      // CTAs finished (the last one resets prog and itself)
 };
+constexpr int kLockWindow = 3;
+constexpr int kLockMaxGroups = 4;  // more groups: waiting for the slowest of them costs more than the re-reads
 }  // namespace
 
 template <int P, int KR>
@@ -130,7 +140,24 @@ __global__ void __launch_bounds__(kPThreads, 1)
     const uint32_t full0 = mapa_shared(smem_u32(full), 0);  // the leader's full barriers
     int s = 0;
     uint32_t ph = 0;
-    for (int64_t t = pair; t < n_tiles; t += npairs) {
+    const bool lock = p.prog != nullptr && gridDim.y > 1 && crank == 0;
+    const int64_t min_rounds = n_tiles / npairs;  // every pair has at least this many rounds
+    int64_t r = 0;
+    for (int64_t t = pair; t < n_tiles; t += npairs, ++r) {
+      if (lock && r >= kLockWindow && r - kLockWindow < min_rounds) {
+        if (lane == 0) {
+          const unsigned need = (unsigned)((r - kLockWindow + 1) * npairs);  // rounds issued per group
+          for (unsigned g = 0; g < gridDim.y; ++g) {
+            for (;;) {
+              unsigned v;
+              asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.prog + g) : "memory");
+              if (v >= need) break;
+              __nanosleep(100);
+            }
+          }
+        }
+        __syncwarp();
+      }
       const int xrow = (int)(t * kPairN) + (int)crank * 128;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty[s], ph ^ 1u);  // the pair's MMA is done with this CTA's slot
@@ -144,6 +171,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
         __syncwarp();
         if (++s == NST) { s = 0; ph ^= 1u; }
       }
+      if (lock && lane == 0) atomicAdd(p.prog + blockIdx.y, 1u);  // this pair issued round r
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer (leader CTA)
@@ -361,6 +389,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
   __syncthreads();
   cluster_sync_all();  // no CTA leaves (or frees TMEM) while its peer may still signal it
+  if (p.prog && threadIdx.x == 0) {  // the last CTA of the launch resets the lockstep counters
+    if (atomicAdd(p.exit_cnt, 1u) == gridDim.x * gridDim.y - 1) {
+      for (unsigned g = 0; g < gridDim.y; ++g) p.prog[g] = 0u;
+      __threadfence();
+      *p.exit_cnt = 0u;
+    }
+  }
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kPTmemCols));
@@ -501,6 +536,10 @@ remoe_status_t tc_pair_scan(TcPlan* t, const uint16_t* q, const float* qnorm, in
     a.smem_bufs = smem_bufs ? 1 : 0;
     a.merge_in_cta = in_cta ? 1 : 0;
     a.dbg = t->kn.dbg;
+    if (ng > 1 && ng <= kLockMaxGroups && t->pair_sync && t->kn.lockstep) {
+      a.prog = t->pair_sync;
+      a.exit_cnt = t->pair_sync + 16;
+    }
     if (t->kn.verbose)
       fprintf(stderr, "[remoe] pair scan grid (%d,%d) stages %d lists/query %d\n", 2 * ppg, ng, nst,
               *lists_per_query);

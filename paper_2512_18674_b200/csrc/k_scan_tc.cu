@@ -976,6 +976,13 @@ remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int 
   if (r != CUDA_SUCCESS) { t->why = "cuTensorMapEncodeTiled failed"; return REMOE_OK; }
   const int64_t n_tiles = (n_rows + kTileN - 1) / kTileN;
   t->grid = (int)(n_tiles < num_sms ? n_tiles : num_sms);
+  if (!t->pair_sync) {
+    if (cudaMalloc(&t->pair_sync, 17 * sizeof(unsigned)) != cudaSuccess ||
+        cudaMemset(t->pair_sync, 0, 17 * sizeof(unsigned)) != cudaSuccess) {
+      cudaGetLastError();
+      t->pair_sync = nullptr;  // the pair scan's groups then run without lockstep
+    }
+  }
   t->ok = true;
   t->why = "";
   return REMOE_OK;
@@ -986,6 +993,8 @@ void tc_plan_destroy(TcPlan* t) {
   if (t->stats_buf) cudaFree(t->stats_buf);
   if (t->trace_buf) cudaFree(t->trace_buf);
   t->stats_buf = t->trace_buf = nullptr;
+  if (t->pair_sync) cudaFree(t->pair_sync);
+  t->pair_sync = nullptr;
 }
 
 template <int M, int P, int KR = 0>

@@ -33,6 +33,7 @@ struct TcKnobs {
   bool no_multicast = false; // REMOE_NO_MULTICAST: no cluster multicast of store tiles
   int epi_sleep = 0;         // REMOE_EPI_SLEEP: epilogue waits with a suspend-time hint
   int dbg = 0;               // REMOE_TC_DBG: experiment bits (wrong results)
+  bool lockstep = false;     // REMOE_PAIR_LOCKSTEP=1: CTA-pair scan query groups in lockstep (k_scan_pair)
   bool stats = false;        // REMOE_TC_STATS: candidate / insert counters (prints, syncs)
   bool trace = false;        // REMOE_TC_TRACE: per-CTA phase stamps (prints, syncs)
   bool verbose = false;      // REMOE_VERBOSE
@@ -46,6 +47,7 @@ struct TcKnobs {
     k.no_multicast = getenv("REMOE_NO_MULTICAST") != nullptr;
     k.epi_sleep = ival("REMOE_EPI_SLEEP", 0);
     k.dbg = ival("REMOE_TC_DBG", 0);
+    k.lockstep = ival("REMOE_PAIR_LOCKSTEP", 0) != 0;
     k.stats = getenv("REMOE_TC_STATS") != nullptr;
     k.trace = getenv("REMOE_TC_TRACE") != nullptr;
     k.verbose = getenv("REMOE_VERBOSE") != nullptr;
@@ -75,6 +77,7 @@ struct TcPlan {
   const uint16_t* xt = nullptr;
   TcKnobs kn;                 // read once at plan creation
   // debug buffers of this plan (REMOE_TC_STATS / REMOE_TC_TRACE), freed by tc_plan_destroy
+  unsigned* pair_sync = nullptr;          // [17] CTA-pair scan group lockstep counters (zeroed, self-resetting)
   unsigned long long* stats_buf = nullptr;
   unsigned long long* trace_buf = nullptr;
 };
