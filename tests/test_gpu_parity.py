@@ -254,6 +254,28 @@ def test_large_dim_reduced_slabs(D):
     s.close()
 
 
+def test_pair_lockstep_same_results(monkeypatch):
+    """REMOE_PAIR_LOCKSTEP=1 (the CTA-pair scan's query groups wait for each other, DESIGN.md
+    §7): only the timing changes -- ids, scores and pred equal the free-running scan bit for
+    bit at B = 600 (3 query groups in one launch), repeated (the counters self-reset)."""
+    c, x, a = store("c2")
+    q = gen.queries(c.store_seed, c.query_seed, c.n, c.dim, 600, mode=1)
+    s_free = make(x, a, max_k=16, max_batch=600)
+    monkeypatch.setenv("REMOE_PAIR_LOCKSTEP", "1")
+    s_lock = make(x, a, max_k=16, max_batch=600)
+    r_free = run(s_free, q, 10)
+    assert s_free.info().last_scan_kernel == KERNELS["pair"]
+    for _ in range(3):
+        r_lock = run(s_lock, q, 10)
+        for u, v in zip(r_free, r_lock):
+            assert np.array_equal(u, v)
+    pick = list(range(0, 600, 40))
+    assert_parity(compare(q[pick], x, a, 10, r_lock[0][pick], r_lock[1][pick], r_lock[2][pick]),
+                  "c2 B=600 pair lockstep (15 sampled)")
+    s_free.close()
+    s_lock.close()
+
+
 def test_chunking_above_max_batch():
     c, x, a = store("c2", 20_000)
     q = gen.queries(c.store_seed, c.query_seed, 20_000, c.dim, 37, mode=1)
