@@ -467,3 +467,35 @@ def test_seeded_large_k(kern, k):
     ids, sc, pred = run(s, q, k)
     assert_parity(compare(q, x, a, k, ids, sc, pred), f"c2[200k] seeded k={k} {kern}")
     assert ids[3, 0] == 16 * 7 and ids[4, 0] == 16 * 7 + 1
+
+
+# ------------------------------------------------------------------ randomized shapes
+
+@pytest.mark.parametrize("case", range(48))
+def test_random_shapes_vs_oracle(case):
+    """Seeded random shapes (store size, D incl. non-multiples of 64 and > 1536, batch across
+    the slab / CTA-pair thresholds, k across the register / buffer top-k boundary, table
+    shape), automatic kernel choice plus one forced kernel each, against the oracle."""
+    rng = np.random.default_rng(1000 + case)
+    n = int(rng.choice([1, 3, 127, 129, 700, 2500, 6000]))
+    D = int(rng.choice([8, 40, 64, 192, 768, 1024, 2048]))
+    B = int(rng.choice([1, 5, 16, 63, 64, 65, 130, 257]))
+    k = int(min(n, rng.choice([1, 2, 7, 16, 31, 33, 64, 100])))
+    L, E = int(rng.integers(1, 6)), int(rng.choice([1, 3, 8, 60]))
+    x = gen.f32_to_bf16_bits(rng.standard_normal((n, D)).astype(np.float32))
+    if n > 3:
+        x[n // 2] = x[n // 3]  # an exact duplicate (tie: lower id first)
+    a = rng.random((n, L, E)).astype(np.float32) + 1e-3
+    a /= a.sum(-1, keepdims=True)
+    q = gen.f32_to_bf16_bits(rng.standard_normal((B, D)).astype(np.float32))
+    q[0] = x[n - 1]  # an exact copy
+    mb = int(max(1, B if case % 4 else rng.integers(1, B + 1)))  # every 4th case: internal chunks
+    s = make(x, a, max_k=max(k, 1), max_batch=mb)
+    ids, sc, pred = run(s, q, k)
+    assert_parity(compare(q, x, a, k, ids, sc, pred),
+                  f"random case {case}: n={n} D={D} B={B} (max_batch {mb}) k={k} L={L} E={E} auto")
+    forced = ["stream", "tc", "pair"][case % 3]
+    if kernel_available(s, forced):
+        ids2, sc2, pred2 = run(s, q, k)
+        assert_parity(compare(q, x, a, k, ids2, sc2, pred2), f"random case {case}: {forced}")
+    s.close()
