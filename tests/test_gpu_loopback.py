@@ -253,3 +253,34 @@ def test_loopback_errors():
         remoe.remoe_loopback_group_destroy(gid)                  # members still built
     s0.close()
     remoe.remoe_loopback_group_destroy(gid)
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_loopback_random(case, monkeypatch):
+    """Seeded random multi-rank cases: G 2-8 uneven shards (some smaller than k), D, B, k,
+    chunking, the fused or the collective exchange (half each), both exchange layouts;
+    against the oracle and across ranks."""
+    rng = np.random.default_rng(500 + case)
+    G = int(rng.integers(2, 9))
+    n = int(rng.choice([G * 3, 500, 4000, 20000]))
+    D = int(rng.choice([64, 256, 768]))
+    B = int(rng.choice([1, 7, 40, 130]))
+    k = int(min(n, rng.choice([1, 5, 16, 40])))
+    mb = int(B if case % 3 else max(1, B // 3))
+    if case % 2:
+        monkeypatch.setenv("REMOE_FUSED_COMM", "1")
+    if case % 5 == 0:
+        monkeypatch.setenv("REMOE_XCHG_AG_MAX", "0")
+    x = gen.f32_to_bf16_bits(rng.standard_normal((n, D)).astype(np.float32))
+    a = rng.random((n, 3, 8)).astype(np.float32) + 1e-3
+    a /= a.sum(-1, keepdims=True)
+    qb = gen.f32_to_bf16_bits(rng.standard_normal((B, D)).astype(np.float32))
+    g = group(x, a, G, max_k=max(k, 1), max_batch=mb)
+    for _ in range(2):  # a second query: replays / advancing sequence numbers
+        ids, sc, pred = run_group(g, qb, k)
+    assert g.ranks[0].info().fused_exchange == (case % 2)
+    g.close()
+    check_ranks_identical(ids, sc, pred)
+    rep = compare(qb, x, a, k, ids[0], sc[0], pred[0])
+    log_report(f"loopback random {case}: G={G} n={n} D={D} B={B} mb={mb} k={k} fused={case % 2}", rep)
+    assert rep.ok(), "\n".join(rep.failures[:20])
