@@ -1122,9 +1122,9 @@ static remoe_status_t check_query(remoe_sps* h, const uint16_t* q, int32_t B, in
   return REMOE_OK;
 }
 
-// The device-buffer query of one chunk (world == 1) through a cached CUDA graph: captured
-// once per (buffers, B, k, kernel choice), replayed as one launch on the library stream,
-// ordered after the caller's earlier work and before its later work by two events.
+// The device-buffer query of one chunk through a cached CUDA graph: captured once per
+// (buffers, B, k, kernel choice) on the library stream, replayed as one launch on the
+// caller's stream.
 static remoe_status_t query_device_graph(remoe_sps* h, const uint16_t* q, int B, int k, int64_t* ids,
                                          float* scores, float* pred, cudaStream_t caller) {
   if (!h->gst) {
@@ -1136,9 +1136,7 @@ static remoe_status_t query_device_graph(remoe_sps* h, const uint16_t* q, int B,
   for (auto& e : h->dg)
     if (e.exec && e.q == q && e.ids == ids && e.scores == scores && e.pred == pred && e.B == B && e.k == k &&
         e.kernel == h->force_kernel) { g = &e; break; }
-  const cudaStream_t st = h->gst;
-  CUDA_TRY(cudaEventRecord(h->gev, caller));
-  CUDA_TRY(cudaStreamWaitEvent(st, h->gev, 0));
+  const cudaStream_t st = h->gst;  // capture only (nothing runs during a capture)
   if (!g) {
     g = &h->dg[0];
     for (auto& e : h->dg)
@@ -1166,9 +1164,9 @@ static remoe_status_t query_device_graph(remoe_sps* h, const uint16_t* q, int B,
     g->scan_kernel = h->last_kernel;
   }
   g->used = ++h->dg_clock;
-  CUDA_TRY(cudaGraphLaunch(g->exec, st));
-  CUDA_TRY(cudaEventRecord(h->gev_done, st));
-  CUDA_TRY(cudaStreamWaitEvent(caller, h->gev_done, 0));
+  // replayed on the caller's stream itself: ordered with its earlier and later work without
+  // the two cross-stream events per query of a launch on a library stream
+  CUDA_TRY(cudaGraphLaunch(g->exec, caller));
   h->last_launches = g->launches;
   h->last_kernel = g->scan_kernel;
   return REMOE_OK;
@@ -1236,8 +1234,8 @@ remoe_status_t remoe_sps_query_group(remoe_group_t g, const uint16_t* q, int32_t
   const int64_t LE = hs[0]->LE;
   int launches = 0;
   if (B <= mb && hs[0]->fused && (!want || xchg_allgather(hs[0], B)) && hs[0]->use_graphs && !hs[0]->prof) {
-    // the whole G-rank sequence as one cached CUDA graph (replayed on the group's stream,
-    // ordered after the caller's earlier work and before its later work by two events)
+    // the whole G-rank sequence as one cached CUDA graph (captured on the group's stream,
+    // replayed on the caller's)
     if (!g->gst) {
       CUDA_TRY(cudaStreamCreateWithFlags(&g->gst, cudaStreamNonBlocking));
       CUDA_TRY(cudaEventCreateWithFlags(&g->gev, cudaEventDisableTiming));
@@ -1252,8 +1250,6 @@ remoe_status_t remoe_sps_query_group(remoe_group_t g, const uint16_t* q, int32_t
     remoe_group::Graph* gr = nullptr;
     for (auto& e : g->graphs)
       if (e.exec && e.q == q && e.B == B && e.k == k && e.bufs == bufs) { gr = &e; break; }
-    CUDA_TRY(cudaEventRecord(g->gev, st));
-    CUDA_TRY(cudaStreamWaitEvent(g->gst, g->gev, 0));
     if (!gr) {
       if (g->graphs.size() >= 8) g->reset_graphs();
       g->graphs.emplace_back();
@@ -1283,9 +1279,7 @@ remoe_status_t remoe_sps_query_group(remoe_group_t g, const uint16_t* q, int32_t
       }
       gr->q = q; gr->bufs = bufs; gr->B = B; gr->k = k; gr->launches = nl;
     }
-    CUDA_TRY(cudaGraphLaunch(gr->exec, g->gst));
-    CUDA_TRY(cudaEventRecord(g->gev_done, g->gst));
-    CUDA_TRY(cudaStreamWaitEvent(st, g->gev_done, 0));
+    CUDA_TRY(cudaGraphLaunch(gr->exec, st));  // on the caller's stream (captured on the group's)
     for (int r = 0; r < G; ++r) hs[r]->last_launches = gr->launches;
     return REMOE_OK;
   }
@@ -1330,9 +1324,7 @@ static remoe_status_t query_host_graph(remoe_sps* h, const uint16_t* q, int B, i
     CUDA_TRY(cudaEventCreateWithFlags(&h->gev, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&h->gev_done, cudaEventDisableTiming));
   }
-  st = h->gst;
-  CUDA_TRY(cudaEventRecord(h->gev, caller));  // after the caller's earlier work on the handle
-  CUDA_TRY(cudaStreamWaitEvent(st, h->gev, 0));
+  st = h->gst;  // capture only; the graph is replayed on the caller's stream
   if (!(g.exec && g.B == B && g.k == k && g.pred == (pred != nullptr))) {
     g.reset();
     CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
@@ -1378,8 +1370,8 @@ static remoe_status_t query_host_graph(remoe_sps* h, const uint16_t* q, int B, i
   CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(g.exec, g.d2h_sc, scores, h->hscores, sb, cudaMemcpyDeviceToHost));
   if (pred)
     CUDA_TRY(cudaGraphExecMemcpyNodeSetParams1D(g.exec, g.d2h_pred, pred, h->hpred, pb, cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaGraphLaunch(g.exec, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaGraphLaunch(g.exec, caller));  // after the caller's earlier work on the handle
+  CUDA_TRY(cudaStreamSynchronize(caller));
   h->last_launches = g.launches;
   return REMOE_OK;
 }
