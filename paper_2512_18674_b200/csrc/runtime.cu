@@ -1388,7 +1388,8 @@ remoe_status_t remoe_sps_query_host(remoe_sps_t h, const uint16_t* q, int32_t B,
   const int mb = h->cfg.max_batch;
   const int D = h->cfg.dim;
   int launches = 0;
-  if (B <= mb && h->cfg.world == 1 && !h->prof && h->use_graphs) {
+  const bool graphable = h->cfg.world == 1 || (h->fused && !h->group && (!pred || xchg_allgather(h, B)));
+  if (B <= mb && graphable && !h->prof && h->use_graphs) {
     remoe_status_t gs = query_host_graph(h, q, B, k, ids, scores, pred, st);
     if (gs != REMOE_ERR_UNSUPPORTED) return gs;  // UNSUPPORTED: pageable buffers -> direct path
   }
