@@ -3,21 +3,26 @@
 // score_ij = (q_i . x_j) / (|q_i||x_j| + sigma)  (Eq. 11, DESIGN R2),
 // exact per-CTA running top-k per query (BF top-alpha).
 //
-// Shape: D[q, j] = sum_k Q[q, k] X[j, k], a bf16 x bf16 -> fp32
-// contraction with M = queries (64 or 128 per pass), N = 128 store rows per tile,
-// K = D.  Both operands are K-major, exactly as they sit in HBM.
-//   * The query slab (A, M x D) is written into shared memory ONCE per CTA in the
-//     128-byte-swizzled K-major layout and stays resident: the only HBM stream is
-//     the store itself (the path is HBM-bound until B ~ 214).
-//   * Warp 0: TMA producer.  Store tiles [128 rows x 64 elems] (16 KB, SWIZZLE_128B)
-//     stream through an NST-deep mbarrier ring with cp.async.bulk.tensor.2d.
-//   * Warp 1: one thread issues tcgen05.mma.cta_group::1.kind::f16 (4 per K-block),
-//     accumulating into one of two TMEM accumulators (128 fp32 columns each), and
-//     tcgen05.commit's the smem slot / the finished accumulator to mbarriers.
-//   * Warps 2-9: epilogue, one thread per (query, tile parity).  tcgen05.ld.32x32b.x32 gives thread (quarter w, lane t)
-//     query m's scores for 32 consecutive store rows; Eq. 11 scaling, key packing and
-//     a register-threshold compare per score; rare inserts go to the thread's private
-//     candidate buffer (LaneTopk, common.cuh).
+// Shape (DESIGN.md §7 "k_scan_tc"): D[q, j] = sum_k Q[q, k] X[j, k], a bf16 x bf16 -> fp32
+// contraction with M = queries (64, or 128 when D <= 576), N = 128 store rows per tile,
+// K = D.  Both operands are K-major.  One persistent CTA per SM, 11 warps:
+//   * The query slab (A) is written into shared memory ONCE per CTA in the 128-byte-
+//     swizzled K-major layout and stays resident (only the 8-row atoms a single slab needs;
+//     max_qps rows when D > 1536): the only HBM stream is the store itself.  The query
+//     norms (S1) are computed from it in the prologue.
+//   * Warp 0: producer.  The build-time tiled copy of the store (16 KB boxes already in the
+//     UMMA layout) streams through an NST-deep mbarrier ring with 1-D cp.async.bulk
+//     (multicast across a cluster of query slabs); seeding sample tiles come first.
+//   * Warp 1: one thread issues tcgen05.mma.cta_group::1.kind::f16 (4 per K-block) into one
+//     of four TMEM accumulators (128 fp32 columns each), bulk-copies the tile's x-norms next
+//     to it, and tcgen05.commit's the smem slot / the finished accumulator to mbarriers.
+//   * Warps 2-9: epilogue, one thread per (query, tile parity).  tcgen05.ld.32x32b.x32 gives
+//     thread (quarter w, lane t) its query's dots for 32 consecutive store rows; a branch-free
+//     conservative prefilter against the state's threshold, exact keys and inserts only for
+//     the rare candidates (RegTopk for k <= 32, LaneTopk buffers above; common.cuh).
+//   * Warp 10: threshold seeding (the r-th largest published sample key per query, a strict
+//     lower bound of the final k-th best), then the broker that mirrors the shared global
+//     thresholds into shared memory for the epilogue.
 // The dot for (q, row) accumulates K-blocks in ascending order inside the tensor core;
 // it does not depend on the query's batch position, on M, or on the sharding.
 #include <cuda.h>
