@@ -1,6 +1,7 @@
 // k_post.cu -- the small kernels around the scan (sm_100a):
-//   S0/S1 row norms, S4/S5 key-list merge, S6+S7 softmax + gather + weighted
-//   reduce, the multi-GPU winner-row gather, S8 expert plan, build validation.
+//   S0/S1 row norms, S4/S5 key-list merge with fused S6+S7 (softmax + gather + weighted
+//   reduce; merge.cuh), the multi-GPU partial-prediction sum in rank order, the fused
+//   exchange's sequence counter, S8 expert plan, build validation.
 #include "common.cuh"
 #include "host_util.h"
 #include "kernels.h"
