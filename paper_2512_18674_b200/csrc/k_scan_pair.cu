@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int NST = p.n_stages;
-  const int nkb = p.dim / kPBK;
+  const int nkb = (p.dim + kPBK - 1) / kPBK;  // the last K-block's columns past D are TMA zero fill
   uint8_t* sA = smem;                              // [NST][128 queries][128 B] swizzled
   uint8_t* sB = sA + (size_t)NST * kBox;           // [NST][128 rows][128 B] swizzled
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)NST * kBox);

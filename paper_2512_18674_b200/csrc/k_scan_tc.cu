@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int D = p.dim;
-  const int nkb = D / kBlockK;  // host guarantees D % 64 == 0
+  const int nkb = (D + kBlockK - 1) / kBlockK;  // the last K-block is zero-padded when D % 64 != 0
   const int NST = p.n_stages;
   uint8_t* sA = smem;                                   // [nkb][M rows][128 B] swizzled
   const int SR = p.slab_rows;
@@ -219,15 +219,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Q[m][kb*64 + c*8 .. +8] -> sA + kb*SR*128 + m*128 + ((c ^ (m & 7)) * 16)  (SWIZZLE_128B).
     // With SR < M the UMMA's rows SR .. M-1 read past the K-block (other K-blocks or the
     // stage ring): garbage accumulator rows of queries >= nq, which no lane reads.
-    const int chunks = SR * (D / 8);
+    const int cpk = nkb * 8;  // 16-byte chunks per slab row, K-padding included
+    const int chunks = SR * cpk;
     const uint32_t a_s = smem_u32(sA);
     for (int i = threadIdx.x - 32; i < chunks; i += blockDim.x - 32) {
-      const int m = i / (D / 8);  // slab row = query
-      const int cc = i - m * (D / 8);
+      const int m = i / cpk;  // slab row = query
+      const int cc = i - m * cpk;
       const int kb = cc >> 3, c = cc & 7;
       const uint32_t dst = a_s + (uint32_t)(kb * SR * 128 + m * 128 + ((c ^ (m & 7)) << 4));
-      const uint16_t* src = qsl + (size_t)(m < nq ? m : 0) * D + cc * 8;
-      const uint32_t bytes = m < nq ? 16u : 0u;  // src-size 0 -> zero fill
+      const bool real = m < nq && cc < (D >> 3);
+      const uint16_t* src = qsl + (size_t)(real ? m : 0) * D + (real ? cc * 8 : 0);
+      const uint32_t bytes = real ? 16u : 0u;  // src-size 0 -> zero fill (padding rows / columns)
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(bytes)
                    : "memory");
     }
@@ -816,22 +818,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 // xt box (tile, kb) = rows tile*128 .. +127, elements kb*64 .. +63, laid out exactly as
 // the UMMA reads a SWIZZLE_128B K-major operand from a 1024-byte aligned stage: row r at
 // r*128 bytes, its 16-byte chunk c at ((c ^ (r & 7)) * 16).  One thread per 16-byte chunk.
+// Columns past D (when D % 64 != 0) and rows past n_rows are zero.
 __global__ void k_tile_store(const uint4* __restrict__ x, int64_t n_rows, int dim, uint4* __restrict__ xt) {
-  const int cpr = dim / 8;  // 16-byte chunks per row
+  const int cpr = dim / 8;                  // 16-byte chunks per source row
+  const int cpk = ((dim + 63) / 64) * 8;    // ... per tiled row, K-padding included
   const int64_t n_tiles = (n_rows + kTileN - 1) / kTileN;
-  const int64_t total = n_tiles * kTileN * cpr;
+  const int64_t total = n_tiles * kTileN * cpk;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = i / cpr;
-    const int cc = (int)(i - row * cpr);
+    const int64_t row = i / cpk;
+    const int cc = (int)(i - row * cpk);
     const int kb = cc >> 3, c = cc & 7, r = (int)(row % kTileN);
     const int64_t tile = row / kTileN;
-    const uint4 v = row < n_rows ? x[i] : make_uint4(0u, 0u, 0u, 0u);
-    xt[((tile * (cpr >> 3) + kb) * kTileN + r) * 8 + (c ^ (r & 7))] = v;
+    const uint4 v = (row < n_rows && cc < cpr) ? x[row * cpr + cc] : make_uint4(0u, 0u, 0u, 0u);
+    xt[((tile * (cpk >> 3) + kb) * kTileN + r) * 8 + (c ^ (r & 7))] = v;
   }
 }
 
 cudaError_t tc_tile_store(const uint16_t* x, int64_t n_rows, int dim, uint16_t* xt, cudaStream_t st) {
-  if (dim % kBlockK != 0 || n_rows <= 0) return cudaErrorInvalidValue;
+  if (dim % 8 != 0 || n_rows <= 0) return cudaErrorInvalidValue;
   k_tile_store<<<1184, 256, 0, st>>>(reinterpret_cast<const uint4*>(x), n_rows, dim, reinterpret_cast<uint4*>(xt));
   return cudaGetLastError();
 }
@@ -876,7 +880,7 @@ remoe_status_t tc_seed_build(TcSeed* sd, const uint16_t* x, const float* xnorm, 
   const int64_t rows = tiles * kTileN;
   int64_t* d_src = static_cast<int64_t*>(alloc(actx, rows * 8));
   uint16_t* tmp = static_cast<uint16_t*>(alloc(actx, (size_t)rows * dim * 2));
-  sd->xt = static_cast<uint16_t*>(alloc(actx, (size_t)rows * dim * 2));
+  sd->xt = static_cast<uint16_t*>(alloc(actx, (size_t)rows * tc_kpad(dim) * 2));
   sd->xn = static_cast<float*>(alloc(actx, (size_t)rows * 4));
   if (!d_src || !tmp || !sd->xt || !sd->xn) return REMOE_ERR_OOM;
   if (cudaMemcpyAsync(d_src, src.data(), rows * 8, cudaMemcpyHostToDevice, st) != cudaSuccess) return REMOE_ERR_CUDA;
@@ -922,7 +926,7 @@ static int g_max_stages = 0;
 
 // slab_rows: query rows stored per K-block (M for a full slab).
 static size_t tc_smem(int M, int slab_rows, int D, int nst, int buf_bytes) {
-  return (size_t)dyn_smem_pad() + (size_t)(D / kBlockK) * slab_rows * 128 + (size_t)nst * kStageBytes +
+  return (size_t)dyn_smem_pad() + (size_t)(tc_kpad(D) / kBlockK) * slab_rows * 128 + (size_t)nst * kStageBytes +
          (3 * (size_t)nst + 2 * kAcc + 4) * 8 + 4 * kTileN * 4 + (size_t)M * 12 + (size_t)buf_bytes;
 }
 
@@ -949,7 +953,7 @@ remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int 
   t->row_stride = row_stride;
   t->grid = 0;
   t->threads_per_cta_queries = kTcEpilogueThreads;
-  if (dim % kBlockK != 0) { t->why = "D % 64 != 0"; return REMOE_OK; }
+  if (dim % 8 != 0) { t->why = "D % 8 != 0"; return REMOE_OK; }  // D % 64 != 0: the last K-block is zero-padded
   // the resident slab holds max_qps query rows: 64 while that leaves >= 3 stages
   // (D <= 1536), else the largest multiple of 8 that leaves >= 4 (D = 2048: 40, 4096: 16);
   // larger batches take several slabs (or the CTA-pair scan)

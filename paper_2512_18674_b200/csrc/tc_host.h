@@ -106,12 +106,15 @@ struct TcSeedUse {
 remoe_status_t tc_seed_build(TcSeed* sd, const uint16_t* x, const float* xnorm, int64_t n_rows, int dim,
                              cudaStream_t st, void* (*alloc)(void*, size_t), void* actx);
 
-// Writes the tiled, pre-swizzled copy of x [n_rows x dim] (dim % 64 == 0) into xt
+// Writes the tiled, pre-swizzled copy of x [n_rows x dim] (dim % 8 == 0; K zero-padded to a multiple of 64) into xt
 // [ceil(n_rows/128) * 128 * dim] (rows past n_rows are zero).
 cudaError_t tc_tile_store(const uint16_t* x, int64_t n_rows, int dim, uint16_t* xt, cudaStream_t st);
 // 0 if dynamic shared memory starts 1024-byte aligned, else 1024 (probed once per process).
 int dyn_smem_pad();
-inline size_t tc_tiled_bytes(int64_t n_rows, int dim) { return (size_t)((n_rows + 127) / 128) * 128 * dim * 2; }
+// D rounded up to whole 64-element K-blocks: the tensor-core scans zero-pad the
+// contraction (D % 8 == 0 is all the API requires; the zeros add nothing to a dot product)
+inline int tc_kpad(int dim) { return (dim + 63) & ~63; }
+inline size_t tc_tiled_bytes(int64_t n_rows, int dim) { return (size_t)((n_rows + 127) / 128) * 128 * tc_kpad(dim) * 2; }
 
 // row_stride: elements between consecutive rows (default dim; a multiple of dim selects
 // every (row_stride/dim)-th row of the store, e.g. the threshold-seeding sample).

@@ -276,6 +276,31 @@ def test_pair_lockstep_same_results(monkeypatch):
     s_lock.close()
 
 
+@pytest.mark.parametrize("D", [8, 40, 776, 1000])
+def test_dim_not_multiple_of_64_on_tensor_cores(D):
+    """D % 64 != 0 runs on the tensor cores with a zero-padded last K-block (tiled copy and
+    query slab padded; TMA zero fill for the CTA-pair scan): the automatic choice is the
+    tensor-core scan, and every kernel (the streaming one included) matches the oracle."""
+    rng = np.random.default_rng(D)
+    n = 1500
+    x = gen.f32_to_bf16_bits(rng.standard_normal((n, D)).astype(np.float32))
+    a = rng.random((n, 3, 8)).astype(np.float32) + 1e-3
+    a /= a.sum(-1, keepdims=True)
+    for B in (3, 130):
+        q = gen.f32_to_bf16_bits(rng.standard_normal((B, D)).astype(np.float32))
+        q[0] = x[7]
+        s = make(x, a, max_k=32, max_batch=B)
+        ids, sc, pred = run(s, q, 12)
+        assert s.info().last_scan_kernel == (KERNELS["tc"] if B < 128 else KERNELS["pair"])
+        assert ids[0, 0] == 7
+        assert_parity(compare(q, x, a, 12, ids, sc, pred), f"D={D} B={B} auto")
+        for kern in ("stream", "tc", "pair"):
+            if kernel_available(s, kern):
+                r = run(s, q, 12)
+                assert_parity(compare(q, x, a, 12, *r), f"D={D} B={B} {kern}")
+        s.close()
+
+
 def test_chunking_above_max_batch():
     c, x, a = store("c2", 20_000)
     q = gen.queries(c.store_seed, c.query_seed, 20_000, c.dim, 37, mode=1)
