@@ -301,6 +301,27 @@ def test_dim_not_multiple_of_64_on_tensor_cores(D):
         s.close()
 
 
+def test_dim_not_multiple_of_64_seeded():
+    """D = 776 on a 40,000-row store: the seeded paths (the padded tiled sample inside the
+    resident-slab scan at B = 40; the strided-tensor-map seed scan of the CTA-pair scan at
+    B = 200) against the oracle on sampled queries."""
+    rng = np.random.default_rng(776)
+    n, D = 40_000, 776
+    x = gen.f32_to_bf16_bits(rng.standard_normal((n, D)).astype(np.float32))
+    a = rng.random((n, 2, 4)).astype(np.float32) + 1e-3
+    a /= a.sum(-1, keepdims=True)
+    q = gen.f32_to_bf16_bits(rng.standard_normal((200, D)).astype(np.float32))
+    q[3] = x[12345]
+    s = make(x, a, max_k=32, max_batch=200)
+    for B, kern in ((40, "tc"), (200, "pair")):
+        ids, sc, pred = run(s, q[:B], 16)
+        assert s.info().last_scan_kernel == KERNELS[kern]
+        assert ids[3, 0] == 12345
+        pick = list(range(0, B, max(1, B // 12)))
+        assert_parity(compare(q[pick], x, a, 16, ids[pick], sc[pick], pred[pick]), f"D=776 n=40k B={B} seeded")
+    s.close()
+
+
 def test_chunking_above_max_batch():
     c, x, a = store("c2", 20_000)
     q = gen.queries(c.store_seed, c.query_seed, 20_000, c.dim, 37, mode=1)
