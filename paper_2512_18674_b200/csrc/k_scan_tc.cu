@@ -557,6 +557,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // gthr there).  Under a full-bandwidth stream an L2 round trip takes microseconds, and
     // a per-tile load one tile ahead stalled the catch-up after the seed (~3 us per tile).
     long long ep_wait = 0, ep_t0 = 0;  // REMOE_TC_TRACE: tfull wait cycles of the store tiles' loop
+    const bool warp_has_query = __any_sync(kFull, active);
     for (int64_t i = parity; i < n_it; i += 2) {
       const bool smp = i < ns_cta;
       if (p.trace && !smp && ep_t0 == 0) { ep_t0 = clock64(); ep_wait = 0; }
@@ -597,7 +598,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (active && !smp) tk.raise(*reinterpret_cast<volatile unsigned long long*>(pair_thr + m));
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kTileN);
-      if (p.dbg & 2) {  // debug (REMOE_TC_DBG=2): release the accumulator unread (wrong results)
+      // A warp with no query of this launch (batches of <= 48 leave whole lane quarters
+      // empty) releases the accumulator unread: no tcgen05.ld, no prefilter -- its issue
+      // slots go to the warps it shares a scheduler with (the MMA issuer among them).
+      // (REMOE_TC_DBG bit 2, experiment: every warp does so -- wrong results)
+      if (!warp_has_query || (p.dbg & 2)) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
         continue;
