@@ -43,17 +43,19 @@
 namespace remoe {
 
 namespace {
-constexpr int kTileN = 128;          // store rows per tile (UMMA N)
+constexpr int kTileN = 128;          // store rows per tile of the tiled copy (k_tile_store)
+constexpr int kUnitN = 256;          // store rows per scan unit = UMMA N: two consecutive tiles
 constexpr int kBlockK = 64;          // bf16 elements per 128-byte swizzle row
-constexpr int kStageBytes = kTileN * kBlockK * 2;  // 16 KB
+constexpr int kTileBytes = kTileN * kBlockK * 2;   // 16 KB: one tile's K-block
+constexpr int kStageBytes = kUnitN * kBlockK * 2;  // 32 KB: one unit's K-block (its two tiles' boxes)
 constexpr int kThreads = 352;        // 11 warps: TMA, MMA, 8 epilogue, seeding
 constexpr int kSeedWarp = 10;        // computes the seeded thresholds (idle without seeding)
 constexpr int kEpiWarps = 8;
-constexpr int kAcc = 4;              // TMEM accumulator stages
-constexpr int kTmemCols = kAcc * kTileN;
+constexpr int kAcc = 2;              // TMEM accumulator stages (256 fp32 columns each)
+constexpr int kTmemCols = kAcc * kUnitN;
 constexpr int kMaxSmem = 232448;     // 227 KB opt-in
 constexpr int kTraceSlots = 32;     // REMOE_TC_TRACE stamps per CTA
-constexpr int kMaxStages = 12;       // stage ring depth cap (TcKnobs::max_stages may lower it)
+constexpr int kMaxStages = 6;        // stage ring depth cap (TcKnobs::max_stages may lower it)
 
 struct TcArgs {
   const float* xnorm;
@@ -91,10 +93,10 @@ struct TcArgs {
   // are >= that key, so it is a lower bound of the final k-th best (strict after -1).
   // The epilogue never waits for it: the thresholds are read again every tile.
   const uint16_t* seed_xt;   // tiled sample (nullptr: no seeding)
-  const float* seed_xn;      // sample norms [n tiles * 128]
-  int seed_n_stiles;         // sample tiles scanned (a prefix of the segments)
+  const float* seed_xn;      // sample norms [n units * 256]
+  int seed_n_stiles;         // sample units scanned (a prefix of the segments)
   int seed_nseg;
-  int seed_t0[5];            // first sample tile of segment g (seed_t0[nseg] = total)
+  int seed_t0[5];            // first sample unit of segment g (seed_t0[nseg] = total)
   int64_t seed_count[4];     // rows of segment g: store rows off + i * stride, i < count
   int64_t seed_off[4];
   int64_t seed_stride[4];
@@ -141,23 +143,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * NST + 2 * kAcc);
   volatile unsigned& s_epoch = *reinterpret_cast<unsigned*>(bars + 3 * NST + 2 * kAcc + 1);  // free slot before sXn
   unsigned* s_epi_done = reinterpret_cast<unsigned*>(bars + 3 * NST + 2 * kAcc + 1) + 1;  // epilogue warps finished
-  // [kAcc][128] x-norms of the tile in accumulator acc: bulk-copied by the MMA warp with the
-  // tile (completing on tfull[acc]), so the epilogue never waits on a global load for them
+  // [kAcc][256] x-norms of the unit in accumulator acc: bulk-copied by the MMA warp with the
+  // unit (completing on tfull[acc]), so the epilogue never waits on a global load for them
   float* sXn = reinterpret_cast<float*>(bars + ((3 * NST + 2 * kAcc + 2 + 1) & ~1));
   // [M] per-query threshold shared by the two parity states of the CTA (register top-k)
-  unsigned long long* pair_thr = reinterpret_cast<unsigned long long*>(sXn + 4 * kTileN);  // [M]
+  unsigned long long* pair_thr = reinterpret_cast<unsigned long long*>(sXn + kAcc * kUnitN);  // [M]
   float* sQn = reinterpret_cast<float*>(pair_thr + M);  // [M] query norms (p.norms_in_kernel)
   uint64_t* sBuf = reinterpret_cast<uint64_t*>(sQn + M);  // [256][CAP] if p.smem_bufs
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t n_tiles = (p.n_rows + kTileN - 1) / kTileN;
-  // This CTA's tile sequence: its sample tiles (threshold seeding) first, then its store
-  // tiles; the TMA producer, the MMA issuer and the epilogue walk the same sequence.
+  const int64_t n_tiles = (p.n_rows + kTileN - 1) / kTileN;  // 128-row tiles of the tiled copy
+  const int64_t n_units = (p.n_rows + kUnitN - 1) / kUnitN;  // 256-row scan units (tiles 2u, 2u + 1)
+  // This CTA's unit sequence: its sample units (threshold seeding) first, then its store
+  // units; the TMA producer, the MMA issuer and the epilogue walk the same sequence.
   const bool seeding = p.seed_xt != nullptr;
   const int64_t ns_cta = (seeding && p.seed_n_stiles > (int)blockIdx.x)
                              ? (p.seed_n_stiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  const int64_t n_it = ns_cta + (n_tiles - 1 - (int64_t)blockIdx.x) / gridDim.x + 1;  // grid.x <= n_tiles
+  const int64_t n_it = ns_cta + (n_units - 1 - (int64_t)blockIdx.x) / gridDim.x + 1;  // grid.x <= n_units
   auto tile_of = [&](int64_t i) -> int64_t {
     return (int64_t)blockIdx.x + (i < ns_cta ? i : i - ns_cta) * (int64_t)gridDim.x;
   };
@@ -267,29 +270,43 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t ph = 0;
     for (int64_t i = 0; i < n_it; ++i) {
       const bool smp = i < ns_cta;
-      const int64_t t = tile_of(i);
-      // tiled store / sample: box (t, kb) is 16 KB contiguous in HBM, already in the swizzled
-      // UMMA layout, so a 1-D bulk copy streams it (no 128 B-per-row DRAM pattern)
-      const uint16_t* tsrc = smp ? p.seed_xt + (size_t)t * nkb * (kStageBytes / 2)
-                                 : p.xt ? p.xt + (size_t)t * nkb * (kStageBytes / 2) : nullptr;
+      const int64_t u = tile_of(i);
+      // tiled store / sample: box (tile, kb) is 16 KB contiguous in HBM, already in the
+      // swizzled UMMA layout, so 1-D bulk copies stream it (no 128 B-per-row DRAM pattern).
+      // Unit u's K-block kb = the boxes (2u, kb) and (2u + 1, kb) back to back: one 256-row
+      // B operand (the sample is padded to whole units; the store's last unit may hold one tile)
+      const uint16_t* tsrc = smp ? p.seed_xt + (size_t)(2 * u) * nkb * (kTileBytes / 2)
+                                 : p.xt ? p.xt + (size_t)(2 * u) * nkb * (kTileBytes / 2) : nullptr;
+      const bool two = smp || 2 * u + 1 < n_tiles;
+      const size_t second = (size_t)nkb * (kTileBytes / 2);  // tile 2u + 1 in the tiled copy
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty[s], ph ^ 1u);  // this CTA's MMA is done with the slot
         if (lane == 0) {
           if (p.dbg & 32) {  // debug (REMOE_TC_DBG bit 32): no load, the slot is "full" at once (wrong results)
             mbar_arrive(&full[s]);
           } else {
-            mbar_arrive_expect_tx(&full[s], kStageBytes);
-            const uint16_t* src = tsrc ? tsrc + (size_t)kb * (kStageBytes / 2) : nullptr;
+            uint8_t* dst = sB + (size_t)s * kStageBytes;
+            mbar_arrive_expect_tx(&full[s], two ? kStageBytes : kTileBytes);
+            const uint16_t* src = tsrc ? tsrc + (size_t)kb * (kTileBytes / 2) : nullptr;
+            const int r0 = (int)(u * kUnitN);
             if (C == 1) {
-              if (src) bulk_g2s(sB + (size_t)s * kStageBytes, src, kStageBytes, &full[s]);
-              else tma_load_2d(sB + (size_t)s * kStageBytes, &tmap_x, kb * kBlockK, (int)(t * kTileN), &full[s]);
+              if (src) {
+                bulk_g2s(dst, src, kTileBytes, &full[s]);
+                if (two) bulk_g2s(dst + kTileBytes, src + second, kTileBytes, &full[s]);
+              } else {
+                tma_load_2d(dst, &tmap_x, kb * kBlockK, r0, &full[s]);
+                if (two) tma_load_2d(dst + kTileBytes, &tmap_x, kb * kBlockK, r0 + kTileN, &full[s]);
+              }
             } else if (crank == 0) {
               mbar_wait(&cempty[s], ph ^ 1u);  // every CTA of the cluster is done with the slot
-              if (src)
-                bulk_g2s_mc(sB + (size_t)s * kStageBytes, src, kStageBytes, &full[s], (uint16_t)((1u << C) - 1u));
-              else
-                tma_load_2d_mc(sB + (size_t)s * kStageBytes, &tmap_x, kb * kBlockK, (int)(t * kTileN), &full[s],
-                               (uint16_t)((1u << C) - 1u));
+              const uint16_t mc = (uint16_t)((1u << C) - 1u);
+              if (src) {
+                bulk_g2s_mc(dst, src, kTileBytes, &full[s], mc);
+                if (two) bulk_g2s_mc(dst + kTileBytes, src + second, kTileBytes, &full[s], mc);
+              } else {
+                tma_load_2d_mc(dst, &tmap_x, kb * kBlockK, r0, &full[s], mc);
+                if (two) tma_load_2d_mc(dst + kTileBytes, &tmap_x, kb * kBlockK, r0 + kTileN, &full[s], mc);
+              }
             }
           }
         }
@@ -306,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // kind::f16: D fp32 (bit 4), A bf16 (bits 7-9 = 1), B bf16 (bits 10-12 = 1),
     // both K-major, N >> 3 at bit 17, M >> 4 at bit 24
     // (debug REMOE_TC_DBG bit 4: N = 32, a quarter of the MMA work; wrong results)
-    const uint32_t nn = (p.dbg & 4) ? 32u : (uint32_t)kTileN;
+    const uint32_t nn = (p.dbg & 4) ? 32u : (uint32_t)kUnitN;
     const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((nn >> 3) << 17) |
                            ((uint32_t)(M >> 4) << 24);
     // descriptor = ((address >> 4) & 0x3FFF) | constant bits: offsets add in 16-byte units
@@ -331,17 +348,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         int nv;
         const float* src;
         if (smp) {
-          src = p.seed_xn + t * kTileN;
-          nv = kTileN;  // the sample's norms are padded to whole tiles
+          src = p.seed_xn + t * kUnitN;
+          nv = kUnitN;  // the sample's norms are padded to whole units
         } else {
-          src = p.xnorm + t * kTileN;
-          nv = (int)min((int64_t)kTileN, p.n_rows - t * kTileN);
+          src = p.xnorm + t * kUnitN;
+          nv = (int)min((int64_t)kUnitN, p.n_rows - t * kUnitN);
         }
         const uint32_t nb = (uint32_t)((nv * 4 + 15) & ~15);
         mbar_arrive_expect_tx(&tfull[acc], nb);
-        bulk_g2s(sXn + acc * kTileN, src, nb, &tfull[acc]);
+        bulk_g2s(sXn + acc * kUnitN, src, nb, &tfull[acc]);
       }
-      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kTileN);
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * kUnitN);
       uint64_t da = da0;
       for (int kb = 0; kb < nkb; ++kb) {
         c0 = p.trace ? clock64() : 0;
@@ -528,15 +545,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             t0 = p.seed_t0[g]; cnt = p.seed_count[g]; off = p.seed_off[g]; str = p.seed_stride[g];
           }
         }
-        const int64_t li = (t - t0) * kTileN;
-        ti.xn = p.seed_xn + t * kTileN;
-        ti.nvalid = (int)min((int64_t)kTileN, cnt - li);
+        const int64_t li = (t - t0) * kUnitN;
+        ti.xn = p.seed_xn + t * kUnitN;
+        ti.nvalid = (int)min((int64_t)kUnitN, cnt - li);
         ti.gstride = str;
         ti.gbase = p.gid_offset + off + li * str;
       } else {
-        const int64_t row0 = t * kTileN;
+        const int64_t row0 = t * kUnitN;
         ti.xn = p.xnorm + row0;
-        ti.nvalid = (int)min((int64_t)kTileN, p.n_rows - row0);
+        ti.nvalid = (int)min((int64_t)kUnitN, p.n_rows - row0);
         ti.gstride = p.gid_stride;
         ti.gbase = p.gid_offset + row0 * p.gid_stride;
       }
@@ -593,11 +610,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (p.epi_sleep) mbar_wait_sleep(&tfull[acc], aph);
       else mbar_wait(&tfull[acc], aph);
       if (p.trace) ep_wait += clock64() - tw0;
-      const float* xs = sXn + acc * kTileN;  // landed with the tile (tfull)
+      const float* xs = sXn + acc * kUnitN;  // landed with the unit (tfull)
       if (i < 2) TRACE(7);
       if (active && !smp) tk.raise(*reinterpret_cast<volatile unsigned long long*>(pair_thr + m));
       tc_fence_after();
-      const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kTileN);
+      const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kUnitN);
       // A warp with no query of this launch (batches of <= 48 leave whole lane quarters
       // empty) releases the accumulator unread: no tcgen05.ld, no prefilter -- its issue
       // slots go to the warps it shares a scheduler with (the MMA issuer among them).
@@ -611,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---- a sample tile: only the tracker (the store pass scans these rows again)
         if (i < 2) TRACE(16);
 #pragma unroll 1
-        for (int c = 0; c < kTileN / 32; ++c) {
+        for (int c = 0; c < kUnitN / 32; ++c) {
           uint32_t v[32];
           tmem_ld32(tbase + c * 32, v);
           tmem_wait_ld();
@@ -670,7 +687,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
 #pragma unroll 1
-      for (int c = 0; c < kTileN / 32; ++c) {
+      for (int c = 0; c < kUnitN / 32; ++c) {
         uint32_t v[32];
         tmem_ld32(tbase + c * 32, v);
         tmem_wait_ld();
@@ -863,26 +880,26 @@ __global__ void k_gather_sample(const uint4* __restrict__ x, const float* __rest
 remoe_status_t tc_seed_build(TcSeed* sd, const uint16_t* x, const float* xnorm, int64_t n_rows, int dim,
                              cudaStream_t st, void* (*alloc)(void*, size_t), void* actx) {
   // segments: rows 64j, 64j+32, 32j+16, 16j+8 (a prefix of g + 1 segments = every
-  // (64 >> g)-th row), each padded to whole 128-row tiles
+  // (64 >> g)-th row), each padded to whole 256-row scan units
   static const int64_t off[4] = {0, 32, 16, 8}, stride[4] = {64, 64, 32, 16};
   sd->n_seg = 0;
-  int64_t tiles = 0;
+  int64_t units = 0;
   std::vector<int64_t> src;
   for (int g = 0; g < 4; ++g) {
     const int64_t cnt = n_rows > off[g] ? (n_rows - off[g] + stride[g] - 1) / stride[g] : 0;
     if (cnt == 0) break;
-    sd->seg_t0[g] = (int)tiles;
+    sd->seg_t0[g] = (int)units;
     sd->seg_count[g] = cnt;
     sd->seg_off[g] = off[g];
     sd->seg_stride[g] = stride[g];
-    const int64_t nt = (cnt + kTileN - 1) / kTileN;
-    for (int64_t i = 0; i < nt * kTileN; ++i) src.push_back(i < cnt ? off[g] + i * stride[g] : -1);
-    tiles += nt;
+    const int64_t nt = (cnt + kUnitN - 1) / kUnitN;  // whole scan units (two tiled-copy tiles each)
+    for (int64_t i = 0; i < nt * kUnitN; ++i) src.push_back(i < cnt ? off[g] + i * stride[g] : -1);
+    units += nt;
     sd->n_seg = g + 1;
   }
-  sd->seg_t0[sd->n_seg] = (int)tiles;
+  sd->seg_t0[sd->n_seg] = (int)units;
   if (sd->n_seg == 0) return REMOE_OK;
-  const int64_t rows = tiles * kTileN;
+  const int64_t rows = units * kUnitN;
   int64_t* d_src = static_cast<int64_t*>(alloc(actx, rows * 8));
   uint16_t* tmp = static_cast<uint16_t*>(alloc(actx, (size_t)rows * dim * 2));
   sd->xt = static_cast<uint16_t*>(alloc(actx, (size_t)rows * tc_kpad(dim) * 2));
@@ -932,12 +949,12 @@ static int g_max_stages = 0;
 // slab_rows: query rows stored per K-block (M for a full slab).
 static size_t tc_smem(int M, int slab_rows, int D, int nst, int buf_bytes) {
   return (size_t)dyn_smem_pad() + (size_t)(tc_kpad(D) / kBlockK) * slab_rows * 128 + (size_t)nst * kStageBytes +
-         (3 * (size_t)nst + 2 * kAcc + 4) * 8 + 4 * kTileN * 4 + (size_t)M * 12 + (size_t)buf_bytes;
+         (3 * (size_t)nst + 2 * kAcc + 4) * 8 + (size_t)kAcc * kUnitN * 4 + (size_t)M * 12 + (size_t)buf_bytes;
 }
 
 static int tc_stages(int M, int D, int buf_bytes, int slab_rows = 0) {
   const long avail = (long)kMaxSmem - (long)tc_smem(M, slab_rows > 0 ? slab_rows : M, D, 0, buf_bytes);
-  const long n = avail / (kStageBytes + 24);  // a stage: its 16 KB + three mbarriers (full, empty, cempty)
+  const long n = avail / (kStageBytes + 24);  // a stage: its 32 KB + three mbarriers (full, empty, cempty)
   const int cap = g_max_stages > 0 ? g_max_stages : kMaxStages;
   return (int)(n > cap ? cap : n);
 }
@@ -959,14 +976,12 @@ remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int 
   t->grid = 0;
   t->threads_per_cta_queries = kTcEpilogueThreads;
   if (dim % 8 != 0) { t->why = "D % 8 != 0"; return REMOE_OK; }  // D % 64 != 0: the last K-block is zero-padded
-  // the resident slab holds max_qps query rows: 64 while that leaves >= 3 stages
-  // (D <= 1536), else the largest multiple of 8 that leaves >= 4 (D = 2048: 40, 4096: 16);
+  // the resident slab holds max_qps query rows: 64 while that leaves >= 2 stages of 32 KB
+  // (D <= 1280), else the largest multiple of 8 that does (D = 1536: 48, 2048: 40, 4096: 16);
   // larger batches take several slabs (or the CTA-pair scan)
   t->max_qps = 0;
-  if (tc_stages(64, dim, 0, 64) >= 3) t->max_qps = 64;
-  else
-    for (int sr = 56; sr >= 8 && t->max_qps == 0; sr -= 8)
-      if (tc_stages(64, dim, 0, sr) >= 4) t->max_qps = sr;
+  for (int sr = 64; sr >= 8 && t->max_qps == 0; sr -= 8)
+    if (tc_stages(64, dim, 0, sr) >= 2) t->max_qps = sr;
   if (t->max_qps == 0) { t->why = "even an 8-query slab does not fit shared memory"; return REMOE_OK; }
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q{};
@@ -988,8 +1003,8 @@ remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int 
                                    t->kn.promotion(),
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) { t->why = "cuTensorMapEncodeTiled failed"; return REMOE_OK; }
-  const int64_t n_tiles = (n_rows + kTileN - 1) / kTileN;
-  t->grid = (int)(n_tiles < num_sms ? n_tiles : num_sms);
+  const int64_t n_units = (n_rows + kUnitN - 1) / kUnitN;
+  t->grid = (int)(n_units < num_sms ? n_units : num_sms);
   if (!t->pair_sync) {
     if (cudaMalloc(&t->pair_sync, 17 * sizeof(unsigned)) != cudaSuccess ||
         cudaMemset(t->pair_sync, 0, 17 * sizeof(unsigned)) != cudaSuccess) {
@@ -1064,16 +1079,16 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
                        uint64_t* cand_buf, unsigned long long* gthr, uint64_t* lists, cudaStream_t st,
                        int* launches, int* lists_per_query, const TcSeedUse* seed, bool norms_in_kernel) {
   if (!t->ok) return REMOE_ERR_UNSUPPORTED;
-  // M = 128 when the 128-query slab still leaves >= 4 stages, else 64.  Candidate
-  // buffers go to shared memory when that still leaves >= 4 stages.
-  const int M = tc_stages(128, t->dim, 0) >= 4 ? 128 : 64;
+  // M = 128 when the 128-query slab still leaves >= 2 stages (64 KB), else 64.  Candidate
+  // buffers go to shared memory when that still leaves >= 2 stages.
+  const int M = tc_stages(128, t->dim, 0) >= 2 ? 128 : 64;
   const int QS = M == 128 ? 128 : t->max_qps;  // queries per slab
   const int buf_bytes = k <= 32 ? 0 : kTcEpilogueThreads * 32 * topk_P(k) * 8;
   // a single slab stores only the 8-row atoms its queries need (more stages for small B)
   const int n_slabs_all = (bc + QS - 1) / QS;
   const TcKnobs& kn = t->kn;
   const int SR = (n_slabs_all == 1 && !(kn.full_slab && QS == M)) ? ((bc + 7) / 8) * 8 : QS;
-  const bool smem_bufs = k > 32 && tc_stages(M, t->dim, buf_bytes, SR) >= 4 && !kn.global_bufs;
+  const bool smem_bufs = k > 32 && tc_stages(M, t->dim, buf_bytes, SR) >= 2 && !kn.global_bufs;
   int nst = tc_stages(M, t->dim, smem_bufs ? buf_bytes : 0, SR);
   if (kn.stages >= 2 && kn.stages < nst) nst = kn.stages;
   // register top-k merges its two parity states in-CTA when the stage ring can hold them
@@ -1152,8 +1167,8 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
       cudaStreamSynchronize(st);
       unsigned long long t0 = ~0ull;
       for (int c = 0; c < n_cta; ++c) if (h[c * kTraceSlots] && h[c * kTraceSlots] < t0) t0 = h[c * kTraceSlots];
-      fprintf(stderr, "[remoe] tc trace (us from first CTA start; CTA 0 | max over CTAs): nq %d k %d tiles %lld\n",
-              a.nq, k, (long long)((n_rows + kTileN - 1) / kTileN));
+      fprintf(stderr, "[remoe] tc trace (us from first CTA start; CTA 0 | max over CTAs): nq %d k %d units %lld\n",
+              a.nq, k, (long long)((n_rows + kUnitN - 1) / kUnitN));
       const char* names[22] = {"start", "setup", "slab", "seed publish", "", "mma tile0 commit",
                                "epi pdl_wait", "epi first tfull", "epi loop done", "end", "seed ready", "", "", "", "",
                                "", "sample tile start", "sample tile end", "seedw pdl_wait", "seedw keys seen", "seedw done", ""};

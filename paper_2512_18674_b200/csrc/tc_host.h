@@ -86,7 +86,7 @@ struct TcPlan {
 // row (s = 64, 32, 16, 8 are prefixes of 1..4 segments), built once per handle.
 struct TcSeed {
   int n_seg = 0;
-  int seg_t0[5] = {0, 0, 0, 0, 0};   // first sample tile of segment g; seg_t0[n_seg] = tiles
+  int seg_t0[5] = {0, 0, 0, 0, 0};   // first sample unit (256 rows) of segment g; seg_t0[n_seg] = units
   int64_t seg_count[4] = {0, 0, 0, 0}, seg_off[4] = {0, 0, 0, 0}, seg_stride[4] = {0, 0, 0, 0};
   uint16_t* xt = nullptr;            // tiled sample [tiles][D/64][16 KB]
   float* xn = nullptr;               // its norms [tiles * 128] (padding rows: 1)
