@@ -307,9 +307,11 @@ REMOE_API remoe_status_t remoe_sps_get_info(remoe_sps_t h, remoe_sps_info_t* inf
 
 /* Force the scan kernel: 0 auto (default), 1 streaming, 2 tensor core (resident query slab),
  * 3 tensor core on CTA pairs (the large-batch GEMM tiling).  Auto picks 3 for batches of
- * at least 128 queries (REMOE_PAIR_MIN_B overrides), else 2 (above D = 1536 the resident
- * slab holds fewer queries -- 40 at D = 2048, 16 at 4096 -- and larger batches take
- * several slabs; D % 64 != 0 zero-pads the last K-block).  1 runs only when forced.
+ * at least 128 queries -- on a shard of >= 16 x 256 rows per SM already for any batch past
+ * one resident slab (65 at D = 1024) -- (REMOE_PAIR_MIN_B overrides), else 2 (above
+ * D = 1280 the resident slab holds fewer queries -- 48 at D = 1536, 40 at 2048, 16 at
+ * 4096 -- and larger batches take several slabs; D % 64 != 0 zero-pads the last K-block).
+ * 1 runs only when forced.
  * Also settable with the environment variable REMOE_FORCE_KERNEL=stream|tc|pair.
  * INVALID_ARG for other values, UNSUPPORTED when the kernel cannot serve this store. */
 REMOE_API remoe_status_t remoe_sps_set_kernel(remoe_sps_t h, int32_t which);

@@ -1074,6 +1074,10 @@ static cudaError_t launch_tc_m(const TcPlan* t, const TcArgs& a, dim3 g, cudaStr
   return cudaErrorInvalidValue;
 }
 
+int tc_single_slab_max(const TcPlan* t) {
+  return !t->ok ? 0 : tc_stages(128, t->dim, 0) >= 2 ? 128 : t->max_qps;
+}
+
 remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc, int k, float sigma,
                        const float* xnorm, int64_t n_rows, int64_t gid_offset, int64_t gid_stride,
                        uint64_t* cand_buf, unsigned long long* gthr, uint64_t* lists, cudaStream_t st,

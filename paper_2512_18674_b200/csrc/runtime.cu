@@ -526,7 +526,13 @@ static remoe_status_t build_local(remoe_sps* h, const uint16_t* emb, const float
   if (const char* e = getenv("REMOE_SEED_SEGS")) h->seed_segs = std::max(0, std::min(4, atoi(e)));
   if (const char* e = getenv("REMOE_SEED_MIN_B")) h->seed_min_b = atoi(e);
   if (const char* e = getenv("REMOE_SEED_KS")) h->seed_ks = std::max(0, std::min(32, atoi(e)));
-  if (const char* e = getenv("REMOE_PAIR_MIN_B")) h->pair_min_b = atoi(e);
+  if (const char* e = getenv("REMOE_PAIR_MIN_B")) {
+    h->pair_min_b = atoi(e);
+  } else if (h->tc.ok && h->tc.grid > 0 &&
+             c.n_local >= (int64_t)remoe::kPairLargeUnits * 256 * h->tc.grid) {
+    // a large shard: batches past one resident slab go to the CTA-pair scan
+    h->pair_min_b = std::min(remoe::kPairMinB, remoe::tc_single_slab_max(&h->tc) + 1);
+  }
   if (const char* e = getenv("REMOE_NO_GRAPH")) h->use_graphs = atoi(e) == 0;
   if (h->tc.kn.trace || h->tc.kn.stats) h->use_graphs = false;  // debug knobs read back and print per launch
   if (const char* e = getenv("REMOE_XCHG_AG_MAX")) h->xchg_ag_max = (size_t)std::max(0LL, atoll(e));

@@ -134,12 +134,17 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
 // Large batches: the CTA-pair (cta_group::2) GEMM-tiled scan (k_scan_pair.cu), same
 // output contract as tc_scan; 256 queries per pair.
 bool tc_pair_usable(const TcPlan* t);
+// queries one resident-slab launch keeps in a single slab (128 for D <= 576, else max_qps)
+int tc_single_slab_max(const TcPlan* t);
 remoe_status_t tc_pair_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc, int k, float sigma,
                             const float* xnorm, int64_t n_rows, int64_t gid_offset, int64_t gid_stride,
                             uint64_t* cand_buf, unsigned long long* gthr, uint64_t* lists, cudaStream_t st,
                             int* launches, int* lists_per_query);
 // Batches of at least this many queries use the pair scan (REMOE_PAIR_MIN_B overrides).
 constexpr int kPairMinB = 128;
+// a shard of >= kPairLargeUnits 256-row units per CTA sends every multi-slab batch to the
+// CTA-pair scan (c3 B = 72-120: 11% faster; on c2-size stores the pair's fixed costs lose)
+constexpr int kPairLargeUnits = 16;
 
 // Largest lists_per_query tc_scan can produce (workspace sizing).
 constexpr int kTcMaxStatesPerCta = 2;

@@ -463,6 +463,28 @@ def test_c3_full_size_mixed_queries():
     s.close()
 
 
+def test_c3_past_one_slab_auto_pair():
+    """c3 (a shard of >= 16 x 256 rows per SM): a batch past one resident slab (B = 96) goes
+    to the CTA-pair scan automatically (kPairLargeUnits); the pair scan and
+    the two-slab resident scan (forced) both match the oracle on 12 sampled queries."""
+    c, x, a = store("c3")
+    B = 96
+    q = gen.queries(c.store_seed, c.query_seed, c.n, c.dim, B, mode=1)
+    s = make(x, a, max_k=c.k, max_batch=256)
+    ids, sc, pred = run(s, q, c.k)
+    assert s.info().last_scan_kernel == KERNELS["pair"]
+    pick = list(range(0, B, 8))
+    o = oracle_run(q[pick], x, a, c.k)
+    assert_parity(compare(q[pick], x, a, c.k, ids[pick], sc[pick], pred[pick], oracle_out=o),
+                  "c3 B=96 auto (pair, 12 sampled)")
+    s.set_kernel(KERNELS["tc"])
+    ids2, sc2, pred2 = run(s, q, c.k)
+    assert s.info().last_scan_kernel == KERNELS["tc"]
+    assert_parity(compare(q[pick], x, a, c.k, ids2[pick], sc2[pick], pred2[pick], oracle_out=o),
+                  "c3 B=96 tc two slabs (12 sampled)")
+    s.close()
+
+
 # ------------------------------------------------------------------ BASELINE c4 and c5 (sampled)
 
 def test_c4_full_size_sampled():
