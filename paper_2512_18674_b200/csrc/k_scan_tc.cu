@@ -4,20 +4,24 @@
 // exact per-CTA running top-k per query (BF top-alpha).
 //
 // Shape (DESIGN.md §7 "k_scan_tc"): D[q, j] = sum_k Q[q, k] X[j, k], a bf16 x bf16 -> fp32
-// contraction with M = queries (64, or 128 when D <= 576), N = 128 store rows per tile,
-// K = D.  Both operands are K-major.  One persistent CTA per SM, 11 warps:
+// contraction with M = queries (64, or 128 when D <= 576), N = 256 store rows per scan
+// unit (two consecutive 128-row tiles of the tiled copy: half the MMA instructions per
+// store byte of N = 128, whose issue loop co-limited the stream), K = D.  Both operands
+// are K-major.  One persistent CTA per SM, 11 warps:
 //   * The query slab (A) is written into shared memory ONCE per CTA in the 128-byte-
 //     swizzled K-major layout and stays resident (only the 8-row atoms a single slab needs;
 //     max_qps rows when D > 1536): the only HBM stream is the store itself.  The query
 //     norms (S1) are computed from it in the prologue.
 //   * Warp 0: producer.  The build-time tiled copy of the store (16 KB boxes already in the
-//     UMMA layout) streams through an NST-deep mbarrier ring with 1-D cp.async.bulk
-//     (multicast across a cluster of query slabs); seeding sample tiles come first.
+//     UMMA layout) streams through an NST-deep ring of 32 KB stages (a unit's K-block: its
+//     two tiles' boxes back to back) with 1-D cp.async.bulk (multicast across a cluster of
+//     query slabs); seeding sample units come first.
 //   * Warp 1: one thread issues tcgen05.mma.cta_group::1.kind::f16 (4 per K-block) into one
-//     of four TMEM accumulators (128 fp32 columns each), bulk-copies the tile's x-norms next
+//     of two TMEM accumulators (256 fp32 columns each), bulk-copies the unit's x-norms next
 //     to it, and tcgen05.commit's the smem slot / the finished accumulator to mbarriers.
 //   * Warps 2-9: epilogue, one thread per (query, tile parity).  tcgen05.ld.32x32b.x32 gives
-//     thread (quarter w, lane t) its query's dots for 32 consecutive store rows; a branch-free
+//     thread (quarter w, lane t) its query's dots for 32 consecutive store rows (8 chunks
+//     per unit); a branch-free
 //     conservative prefilter against the state's threshold, exact keys and inserts only for
 //     the rare candidates (RegTopk for k <= 32, LaneTopk buffers above; common.cuh).
 //   * Warp 10: threshold seeding (the r-th largest published sample key per query, a strict
