@@ -1089,8 +1089,8 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
   if (!t->ok) return REMOE_ERR_UNSUPPORTED;
   // M = 128 when the 128-query slab still leaves >= 2 stages (64 KB), else 64.  Candidate
   // buffers go to shared memory when that still leaves >= 2 stages.
-  const int M = tc_stages(128, t->dim, 0) >= 2 ? 128 : 64;
-  const int QS = M == 128 ? 128 : t->max_qps;  // queries per slab
+  const int QS = tc_single_slab_max(t);  // queries per slab
+  const int M = QS == 128 ? 128 : 64;    // max_qps <= 64
   const int buf_bytes = k <= 32 ? 0 : kTcEpilogueThreads * 32 * topk_P(k) * 8;
   // a single slab stores only the 8-row atoms its queries need (more stages for small B)
   const int n_slabs_all = (bc + QS - 1) / QS;

@@ -190,6 +190,7 @@ struct remoe_sps {
   remoe::TcSeed seed_store{};
   bool seed_inkernel = true;  // REMOE_SEED_INKERNEL=0: the separate seed-scan launch instead (A/B)
   int seed_segs = 0;          // REMOE_SEED_SEGS: sample segments used by the in-kernel seed (0: by k)
+  int seed_units_per_k = 2;   // REMOE_SEED_UNITS_PER_K: sample units the in-kernel seed wants per k
   uint64_t* seed_top = nullptr;
   // -1 auto: seed when k >= kSeedMinK or B >= seed_min_b; 1 always (REMOE_SEED=1); 0 never
   // (REMOE_SEED=0).  Without a seed every top-k state (a CTA's rows for one query) starts
@@ -524,6 +525,7 @@ static remoe_status_t build_local(remoe_sps* h, const uint16_t* emb, const float
   if (const char* e = getenv("REMOE_SEED")) h->seed_mode = atoi(e) != 0 ? 1 : 0;
   if (const char* e = getenv("REMOE_SEED_INKERNEL")) h->seed_inkernel = atoi(e) != 0;
   if (const char* e = getenv("REMOE_SEED_SEGS")) h->seed_segs = std::max(0, std::min(4, atoi(e)));
+  if (const char* e = getenv("REMOE_SEED_UNITS_PER_K")) h->seed_units_per_k = std::max(1, std::min(8, atoi(e)));
   if (const char* e = getenv("REMOE_SEED_MIN_B")) h->seed_min_b = atoi(e);
   if (const char* e = getenv("REMOE_SEED_KS")) h->seed_ks = std::max(0, std::min(32, atoi(e)));
   if (const char* e = getenv("REMOE_PAIR_MIN_B")) {
@@ -812,15 +814,16 @@ static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k,
     const remoe::TcSeed& ss = h->seed_store;
     if (which == 2 && seed && ss.n_seg > 0 && h->seed_inkernel) {
       // Each state publishes its best sample key (h = 1) and the threshold is the k-th largest
-      // of them (r = k): the sample needs >= 2k tiles, so the prefix grows with k (every 64th
-      // row, then 32nd, 16th, 8th; REMOE_SEED_SEGS overrides the segment count).  One key per
-      // 128-row block of a random-order sample: the k-th largest block maximum is about the
-      // k-th best row of the sample.
+      // of them (r = k): the sample needs >= k units (seed_units_per_k * k wanted), so the
+      // prefix grows with k (every 64th row, then 32nd, 16th, 8th; REMOE_SEED_SEGS overrides
+      // the segment count).  One key per 256-row unit of a random-order sample: the k-th
+      // largest unit maximum is about the k-th best row of the sample.
+      const int want = h->seed_units_per_k * k;
       int nseg = 1;
-      while (nseg < ss.n_seg && ss.seg_t0[nseg] < 2 * k) ++nseg;
+      while (nseg < ss.n_seg && ss.seg_t0[nseg] < want) ++nseg;
       if (h->seed_segs > 0) nseg = std::min(h->seed_segs, ss.n_seg);
       const int ntl = ss.seg_t0[nseg];
-      if (ntl >= 2 * k) {
+      if (ntl >= want) {
         su.store = &ss;
         su.n_stiles = ntl;
         su.h = 1;
