@@ -977,7 +977,7 @@ remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int 
   t->n_rows = n_rows;
   t->dim = dim;
   t->row_stride = row_stride;
-  t->grid = 0;
+  t->grid = t->grid_units = 0;
   t->threads_per_cta_queries = kTcEpilogueThreads;
   if (dim % 8 != 0) { t->why = "D % 8 != 0"; return REMOE_OK; }  // D % 64 != 0: the last K-block is zero-padded
   // the resident slab holds max_qps query rows: 64 while that leaves >= 2 stages of 32 KB
@@ -1007,8 +1007,9 @@ remoe_status_t tc_plan_create(TcPlan* t, const uint16_t* x, int64_t n_rows, int 
                                    t->kn.promotion(),
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) { t->why = "cuTensorMapEncodeTiled failed"; return REMOE_OK; }
-  const int64_t n_units = (n_rows + kUnitN - 1) / kUnitN;
-  t->grid = (int)(n_units < num_sms ? n_units : num_sms);
+  const int64_t n_tiles = (n_rows + kTileN - 1) / kTileN, n_units = (n_rows + kUnitN - 1) / kUnitN;
+  t->grid = (int)(n_tiles < num_sms ? n_tiles : num_sms);
+  t->grid_units = (int)(n_units < num_sms ? n_units : num_sms);
   if (!t->pair_sync) {
     if (cudaMalloc(&t->pair_sync, 17 * sizeof(unsigned)) != cudaSuccess ||
         cudaMemset(t->pair_sync, 0, 17 * sizeof(unsigned)) != cudaSuccess) {
@@ -1106,8 +1107,8 @@ remoe_status_t tc_scan(TcPlan* t, const uint16_t* q, const float* qnorm, int bc,
   // Query slabs of M: one launch covers up to grid slabs, each slab on grid / slabs CTAs
   // walking the store in the same tile order (L2 sharing of every tile across slabs).
   const int n_slabs = n_slabs_all;
-  const int slabs_per_launch = n_slabs < t->grid ? n_slabs : t->grid;
-  const int ctas_per_slab = t->grid / slabs_per_launch;
+  const int slabs_per_launch = n_slabs < t->grid_units ? n_slabs : t->grid_units;
+  const int ctas_per_slab = t->grid_units / slabs_per_launch;
   *lists_per_query = ctas_per_slab * lists_per_cta;
   for (int sl0 = 0; sl0 < n_slabs; sl0 += slabs_per_launch) {
     const int ns = n_slabs - sl0 < slabs_per_launch ? n_slabs - sl0 : slabs_per_launch;

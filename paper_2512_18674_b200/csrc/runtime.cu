@@ -803,7 +803,7 @@ static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k,
     for (int i = 0; i < h->n_seeds; ++i)
       if (h->seeds[i].stride >= want_stride) si = i;
     const remoe_sps::SeedSample* sd = h->n_seeds > 0 ? &h->seeds[si] : nullptr;
-    const int sg = sd ? sd->tc.grid : 0;
+    const int sg = sd ? (which == 3 ? sd->tc.grid : sd->tc.grid_units) : 0;  // the seed scan's CTAs
     const int lists_min = which == 3 ? std::max(1, (sg / 2) / std::max(1, std::min((bc + 255) / 256, sg / 2)))
                                      : std::max(1, sg / std::max(1, std::min((bc + 63) / 64, sg)));
     int ks_auto = remoe::seed_ks_for(k);

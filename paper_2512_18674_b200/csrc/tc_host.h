@@ -63,9 +63,10 @@ inline int seed_ks_for(int k) { return k <= 32 ? 1 : k <= 64 ? 2 : 4; }
 
 struct TcPlan {
   bool ok = false;            // tensor-core scan usable for this store
-  int max_qps = 64;           // queries per resident slab (64; fewer for D > 1536)
+  int max_qps = 64;           // queries per resident slab (64; fewer for D > 1280)
   const char* why = "not initialised";
-  int grid = 0;               // persistent CTAs
+  int grid = 0;               // persistent CTAs (CTA-pair scan, workspaces): min(128-row tiles, SMs)
+  int grid_units = 0;         // resident-slab scan CTAs: min(256-row units, SMs) <= grid
   int threads_per_cta_queries = 0;  // per-CTA private top-k lanes
   alignas(64) unsigned char tmap_x[128];  // CUtensorMap of the store (bf16 [n][D], K-major)
   const uint16_t* x = nullptr;
