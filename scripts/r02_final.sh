@@ -13,12 +13,12 @@ cap() {  # tag, regex, bench args...
   timeout 400 python bench.py --json-out $out/bench.json "$@" > $out/bench.log 2>&1
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
       --log-file $out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline "$@" > $out/launches.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$rx -s 4 -c 1 -o $out/scan -f \
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$rx" -s 2 -c 1 -o $out/scan -f \
       python bench.py --steps 2 --warmup 3 --no-cpu-baseline "$@" > $out/ncu_full.log 2>&1
 }
 cap c3_b64 k_scan
 cap c2_b16 k_scan --config c2 --batch 16 --no-cpu-baseline
-cap c3_b1024 k_scan_pair --batch 1024 --no-cpu-baseline
+cap c3_b1024 'k_scan_pair<.int.0, .int.16>' --batch 1024 --no-cpu-baseline  # not the seed-scan launch <0, 8>
 cap c4_b1 k_scan --config c4 --batch 1 --k 32 --no-cpu-baseline
 mkdir -p $root/${pre}_extra
 line() { local tag=$1; shift; timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --json-out $root/${pre}_extra/$tag.json "$@" > /dev/null 2>&1; }
