@@ -191,7 +191,8 @@ struct remoe_sps {
   bool seed_inkernel = true;  // REMOE_SEED_INKERNEL=0: the separate seed-scan launch instead (A/B)
   int seed_segs = 0;          // REMOE_SEED_SEGS: sample segments used by the in-kernel seed (0: by k)
   int seed_units_per_k = 0;   // REMOE_SEED_UNITS_PER_K: sample units the in-kernel seed wants per k
-                              // (0: 2 for k <= 64, 1 above -- c3 B = 16/64, k = 128: 0.90/0.83 -> 0.93/0.85)
+                              // (0: 3 for k <= 64, 1 above -- c3 B = 16/64, k = 128: 0.90/0.83 -> 0.93/0.85
+                              // with 1 instead of 2; c2 B = 16/64: 2 -> 3 is 2-3% faster)
   uint64_t* seed_top = nullptr;
   // -1 auto: seed when k >= kSeedMinK or B >= seed_min_b; 1 always (REMOE_SEED=1); 0 never
   // (REMOE_SEED=0).  Without a seed every top-k state (a CTA's rows for one query) starts
@@ -819,12 +820,12 @@ static remoe_status_t stage_scan(remoe_sps* h, const uint16_t* q, int bc, int k,
       // prefix grows with k (every 64th row, then 32nd, 16th, 8th; REMOE_SEED_SEGS overrides
       // the segment count).  One key per 256-row unit of a random-order sample: the k-th
       // largest unit maximum is about the k-th best row of the sample.
-      const int want = (h->seed_units_per_k > 0 ? h->seed_units_per_k : k <= 64 ? 2 : 1) * k;
+      const int want = (h->seed_units_per_k > 0 ? h->seed_units_per_k : k <= 64 ? 3 : 1) * k;
       int nseg = 1;
       while (nseg < ss.n_seg && ss.seg_t0[nseg] < want) ++nseg;
       if (h->seed_segs > 0) nseg = std::min(h->seed_segs, ss.n_seg);
       const int ntl = ss.seg_t0[nseg];
-      if (ntl >= want) {
+      if (ntl >= k) {  // a smaller sample than wanted still seeds (k keys are enough)
         su.store = &ss;
         su.n_stiles = ntl;
         su.h = 1;
