@@ -484,7 +484,8 @@ remoe_status_t tc_pair_scan(TcPlan* t, const uint16_t* q, const float* qnorm, in
   const int D = t->dim;
   const int buf_bytes = k <= 32 ? 0 : kTcEpilogueThreads * 32 * topk_P(k) * 8;
   const bool smem_bufs = k > 32 && pair_stages(buf_bytes) >= 4;
-  const int nst = pair_stages(smem_bufs ? buf_bytes : 0);
+  int nst = pair_stages(smem_bufs ? buf_bytes : 0);
+  if (t->kn.stages >= 2 && t->kn.stages < nst) nst = t->kn.stages;  // REMOE_TC_STAGES (experiments)
   const int KR = k <= 1 ? 1 : k <= 2 ? 2 : k <= 4 ? 4 : k <= 8 ? 8 : k <= 16 ? 16 : 32;
   const bool in_cta = k <= 32 && (size_t)nst * kBox >= (size_t)kTcEpilogueThreads * KR * 8;
   const int lists_per_cta = in_cta ? 1 : 2;
