@@ -162,11 +162,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   // This CTA's unit sequence: its sample units (threshold seeding) first, then its store
   // units; the TMA producer, the MMA issuer and the epilogue walk the same sequence.
   const bool seeding = p.seed_xt != nullptr;
-  const int64_t ns_cta = (seeding && p.seed_n_stiles > (int)blockIdx.x)
-                             ? (p.seed_n_stiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  const int64_t n_it = ns_cta + (n_units - 1 - (int64_t)blockIdx.x) / gridDim.x + 1;  // grid.x <= n_units
+  // Store unit u goes to CTA u mod grid, so the first n_units mod grid CTAs hold one unit
+  // more; sample unit j goes to CTA (n_units + j) mod grid, i.e. to the others first, which
+  // evens the CTAs' total work (c3: 28 -> 27 units on the busiest CTAs).  (REMOE_TC_DBG bit
+  // 512, experiment: sample unit j on CTA j.)
+  const int G = (int)gridDim.x;
+  const int srot = (p.dbg & 512) ? 0 : (int)(n_units % G);
+  const int sidx = ((int)blockIdx.x - srot + G) % G;  // this CTA's first sample unit
+  const int64_t ns_cta = (seeding && p.seed_n_stiles > sidx) ? (p.seed_n_stiles - 1 - sidx) / G + 1 : 0;
+  const int64_t n_it = ns_cta + (n_units - 1 - (int64_t)blockIdx.x) / G + 1;  // grid.x <= n_units
   auto tile_of = [&](int64_t i) -> int64_t {
-    return (int64_t)blockIdx.x + (i < ns_cta ? i : i - ns_cta) * (int64_t)gridDim.x;
+    return i < ns_cta ? (int64_t)sidx + i * G : (int64_t)blockIdx.x + (i - ns_cta) * G;
   };
   TRACE(0);
   if (p.trace && threadIdx.x == 0) p.trace[(blockIdx.y * gridDim.x + blockIdx.x) * kTraceSlots + 11] = clock64();
